@@ -1,0 +1,23 @@
+"""paper_2410_18129_b200 -- B200-native batched constant-time Montgomery modexp.
+
+The hot path of arXiv 2410.18129 (truncated batch Montgomery multiplication and
+constant-time fixed-window modular exponentiation) as hand-written sm_100a CUDA
+kernels behind a C-ABI library (include/mpb.h, csrc/), with a thin ctypes
+binding (``paper_2410_18129_b200.mpb``).  ``inputs`` holds the seeded input
+generators shared with the oracle.  The binding is imported lazily so that
+CPU-only tooling (tests of the oracle, the input generators) never needs CUDA.
+"""
+
+__all__ = ["inputs", "mpb"]
+
+
+def __getattr__(name):
+    if name == "mpb":
+        from . import mpb as _m
+
+        return _m
+    if name == "inputs":
+        from . import inputs as _i
+
+        return _i
+    raise AttributeError(name)
