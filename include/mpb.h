@@ -1,0 +1,103 @@
+/*
+ * mpb.h -- C ABI of libmpb.so: batched constant-time Montgomery arithmetic on NVIDIA B200
+ * (sm_100a), the data-parallel hot path of arXiv 2410.18129 (PAPER.md in the reference).
+ *
+ * Numbers.  Unsigned integers in 32-bit limbs, little-endian (a GMP-style
+ * 64-bit little-endian word array is byte-identical).  L = mpb_limbs(bits) = 4*ceil(bits/128)
+ * limbs per operand, R = 2^(32L).  Supported L: 16, 32, 64, 96, 128, 132 (bits 481..512,
+ * 993..1024, 1985..2048, 2945..3072, 3969..4096, 4097..4224); anything else is
+ * MPB_EUNSUPPORTED.
+ *
+ * Layout ("word-sliced", the B200 form of the paper's Table 1 word slicing):
+ * every device array argument below holds `count` operands of `nlimbs` limbs as
+ *     limb i of operand k at  uint32 index  ((i/4)*count + k)*4 + (i%4)
+ * i.e. 16-byte chunks of 4 consecutive limbs, chunk-major, operand-minor: one uint4 load
+ * per thread per chunk, a warp reads 512 contiguous bytes.  mpb_layout_expand/contract
+ * convert from/to the operand-major layout (operand k's limbs contiguous), the paper's
+ * `expand`/`contract`.
+ *
+ * Calls.  All pointers are DEVICE pointers, 16-byte aligned, owned by the caller; the library
+ * never allocates or frees them and keeps no state between calls except the thread-local
+ * error string.  Work is enqueued on `stream` (a cudaStream_t, 0 = legacy default) and the
+ * call returns immediately; kernel faults surface at the caller's next synchronisation.
+ * count == 0 is a no-op returning MPB_OK.  Outputs must not alias inputs.
+ *
+ * Preconditions NOT checked on the device (no host sync; violations give unspecified
+ * output, never a fault): N odd, 1 < N < 2^bits; a, b, base < N; T < N*R; exp < 2^bits;
+ * Nprime == (-N)^-1 mod R; R2 == R^2 mod N.  Modular outputs are canonical, in [0, N),
+ * for both REDC modes; `redc` and `algo` never change a result, only speed.
+ *
+ * Errors.  MPB_EINVAL: null / misaligned / aliasing pointer, redc or algo out of range,
+ * window not in 1..6 (SPEC "shape"/"usage" errors).  MPB_EUNSUPPORTED: bits not compiled
+ * (SPEC "configuration error").  MPB_ECUDA: launch failure; text via mpb_last_error().
+ */
+#ifndef PAPER_2410_18129_MPB_H
+#define PAPER_2410_18129_MPB_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum { MPB_OK = 0, MPB_EINVAL = -1, MPB_EUNSUPPORTED = -2, MPB_ECUDA = -3 } mpb_status;
+enum { MPB_REDC_FULL = 0, MPB_REDC_TRUNCATED = 1 };
+enum { MPB_ALGO_AUTO = 0, MPB_ALGO_SCHOOLBOOK = 1, MPB_ALGO_KARATSUBA = 2 };
+
+/* L(bits) = 4*ceil(bits/128); 0 if bits <= 0. */
+int mpb_limbs(int bits);
+/* 1 if bits maps to a compiled limb count. */
+int mpb_supported(int bits);
+
+/* Layout: operand-major (count x limbs) <-> word-sliced.  limbs % 4 == 0. */
+int mpb_layout_expand(const uint32_t* src_opmajor, uint32_t* dst, size_t count, int limbs, void* stream);
+int mpb_layout_contract(const uint32_t* src, uint32_t* dst_opmajor, size_t count, int limbs, void* stream);
+
+/* c = a*b, c has 2L limbs (word-sliced with 2L limbs).  alg:8SBmul. */
+int mp_batch_mul(const uint32_t* a, const uint32_t* b, uint32_t* c, size_t count, int bits, int algo, void* stream);
+/* c = a^2, c has 2L limbs.  alg:8SBsqu. */
+int mp_batch_sqr(const uint32_t* a, uint32_t* c, size_t count, int bits, int algo, void* stream);
+
+/* c = a*b*R^-1 mod N (canonical).  redc = MPB_REDC_TRUNCATED (alg:trunc_montred)
+ * or MPB_REDC_FULL (alg:8MontRed).  Nprime is the full (-N)^-1 mod R (limb 0 is
+ * the n0' of CIOS).  workspace: mont_batch_workspace(count, bits) bytes of device memory. */
+int mont_batch_mul(const uint32_t* a, const uint32_t* b, const uint32_t* N, const uint32_t* Nprime,
+                   uint32_t* c, size_t count, int bits, int redc, void* workspace, size_t workspace_bytes,
+                   void* stream);
+/* c = a^2*R^-1 mod N (canonical). */
+int mont_batch_sqr(const uint32_t* a, const uint32_t* N, const uint32_t* Nprime, uint32_t* c, size_t count,
+                   int bits, int redc, void* workspace, size_t workspace_bytes, void* stream);
+/* c = T*R^-1 mod N for T < N*R given with 2L limbs (word-sliced with 2L limbs).  alg:montred. */
+int mont_batch_redc(const uint32_t* T, const uint32_t* N, const uint32_t* Nprime, uint32_t* c, size_t count,
+                    int bits, int redc, void* workspace, size_t workspace_bytes, void* stream);
+size_t mont_batch_workspace(size_t count, int bits);
+
+/* out = base^exp mod N, constant-time fixed-window left-to-right exponentiation
+ * (alg:8FWExp): 2^window-entry table in Montgomery form, windows LSB-aligned,
+ * the top partial window selects the start value, then per window `window` Montgomery
+ * squarings, a masked full-table scan and one Montgomery multiplication.
+ * exp has L limbs and `bits` significant bits (zero padded); timing depends on
+ * (count, bits, window, redc) only.  window in 1..6.  exp = 0 gives 1 (0^0 = 1). */
+int mont_batch_modexp_ct(const uint32_t* N, const uint32_t* Nprime, const uint32_t* R2, const uint32_t* base,
+                         const uint32_t* exp, uint32_t* out, size_t count, int bits, int window, int redc,
+                         int algo, void* workspace, size_t workspace_bytes, void* stream);
+size_t mont_batch_modexp_ct_workspace(size_t count, int bits, int window, int algo);
+
+/* Montgomery constants: Nprime = (-N)^-1 mod R, R2 = R^2 mod N ("precomputed values"). */
+int mont_batch_setup(const uint32_t* N, uint32_t* Nprime, uint32_t* R2, size_t count, int bits,
+                     void* workspace, size_t workspace_bytes, void* stream);
+size_t mont_batch_setup_workspace(size_t count, int bits);
+
+/* End-to-end convenience over HOST buffers (operand-major, L limbs each; exp L limbs):
+ * allocates device memory, copies in, runs setup + modexp, copies out, synchronises.
+ * Returns MPB_OK or an error; blocking. */
+int mpb_modexp_host(const uint32_t* N, const uint32_t* base, const uint32_t* exp, uint32_t* out, size_t count,
+                    int bits, int window, int redc, void* stream);
+
+/* Thread-local text of the last error ("" if none). */
+const char* mpb_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

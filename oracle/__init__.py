@@ -188,7 +188,9 @@ def batch_modexp(base: np.ndarray, e: np.ndarray, ebits: int, N: np.ndarray, thr
     """Operand-major uint32 arrays: base, N (count, L); e (count, ceil(ebits/32))."""
     base, e, N = (np.ascontiguousarray(x, dtype=np.uint32) for x in (base, e, N))
     count, L = N.shape
-    assert e.shape == (count, (ebits + 31) // 32)
+    eL = (ebits + 31) // 32
+    assert e.shape[0] == count and e.shape[1] >= eL
+    e = np.ascontiguousarray(e[:, :eL])  # the limbs holding the ebits-bit exponent
     out = np.zeros((count, L), np.uint32)
     th = threads or os.cpu_count() or 1
     if lib().o_batch_modexp(_p(base), _p(e), ebits, _p(N), L, _p(out), count, th) != 0:

@@ -7,17 +7,12 @@ binding (``paper_2410_18129_b200.mpb``).  ``inputs`` holds the seeded input
 generators shared with the oracle.  The binding is imported lazily so that
 CPU-only tooling (tests of the oracle, the input generators) never needs CUDA.
 """
+import importlib
 
 __all__ = ["inputs", "mpb"]
 
 
 def __getattr__(name):
-    if name == "mpb":
-        from . import mpb as _m
-
-        return _m
-    if name == "inputs":
-        from . import inputs as _i
-
-        return _i
+    if name in __all__:
+        return importlib.import_module(f"{__name__}.{name}")
     raise AttributeError(name)

@@ -1,0 +1,360 @@
+// mpb.cu -- kernels and the C ABI (include/mpb.h) of libmpb.so, sm_100a.
+//
+// One thread per operand (the warp is the paper's "batch of 8" widened to 32 lanes,
+// PAPER.md L66-98); operands are word-sliced in HBM so each uint4 access of a warp
+// is 512 contiguous bytes.  See DESIGN.md for the data layout, the per-kernel
+// roofline and the readings of the paper.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/mpb.h"
+#include "launch.h"
+
+#define MPB_DEVI __device__ __forceinline__
+
+using mpb::Launch;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+constexpr int kThreads = 128;
+
+MPB_DEVI size_t tid_global() { return (size_t)blockIdx.x * blockDim.x + threadIdx.x; }
+
+// word-sliced accessor for operand k of an array with `count` operands
+// word i of operand k (32-bit access)
+MPB_DEVI uint32_t word_at(const uint32_t* base, size_t count, size_t k, int i) {
+    return __ldg(base + ((size_t)(i >> 2) * count + k) * 4 + (i & 3));
+}
+
+// ------------------------------------------------------------- layout kernels
+__global__ void k_expand(const uint4* __restrict__ src, uint4* __restrict__ dst, size_t count, int chunks) {
+    const size_t t = tid_global();
+    if (t >= count * (size_t)chunks) return;
+    const size_t q = t / count, k = t % count;
+    dst[q * count + k] = src[k * chunks + q];
+}
+__global__ void k_contract(const uint4* __restrict__ src, uint4* __restrict__ dst, size_t count, int chunks) {
+    const size_t t = tid_global();
+    if (t >= count * (size_t)chunks) return;
+    const size_t q = t / count, k = t % count;
+    dst[k * chunks + q] = src[q * count + k];
+}
+
+// ---------------------------------------------------------------- setup
+// Nprime = (-N)^-1 mod R by word-wise Hensel lifting; R2 = 2^(64L) mod N by doubling.
+// Untimed support kernel (the paper's "precomputed values").  Scratch: A (L+1 words
+// rounded to L+4), X (L) per operand, 32-bit access into the word-sliced layout.
+MPB_DEVI uint32_t* wptr(uint32_t* base, size_t count, size_t k, int i) {
+    return base + ((size_t)(i >> 2) * count + k) * 4 + (i & 3);
+}
+__global__ void k_setup(const uint32_t* __restrict__ N, uint32_t* __restrict__ NP, uint32_t* __restrict__ R2,
+                        size_t count, int L, uint32_t* ws) {
+    const size_t k = tid_global();
+    if (k >= count) return;
+    uint32_t* A = ws;                                  // L + 4 words per operand
+    uint32_t* X = ws + (size_t)(L + 4) * count;       // L words per operand
+    auto n = [&](int i) { return word_at(N, count, k, i); };
+    // n0' = -N0^-1 mod 2^32 (Newton: 5 steps double the correct bits 1 -> 32... start with 3 bits)
+    const uint32_t n0 = n(0);
+    uint32_t inv = n0;  // correct to 3 bits for odd n0
+#pragma unroll
+    for (int it = 0; it < 5; it++) inv *= 2u - n0 * inv;
+    const uint32_t n0p = 0u - inv;
+    // A = 1; for i: x_i = A[i]*n0'; A += x_i * N * 2^(32 i)  (mod R)
+    for (int i = 0; i < L; i++) *wptr(A, count, k, i) = (i == 0);
+    for (int i = 0; i < L; i++) {
+        const uint32_t xi = *wptr(A, count, k, i) * n0p;
+        *wptr(NP, count, k, i) = xi;
+        uint64_t carry = 0;
+        for (int j = 0; i + j < L; j++) {
+            uint32_t* ap = wptr(A, count, k, i + j);
+            const uint64_t t = (uint64_t)xi * n(j) + *ap + carry;
+            *ap = (uint32_t)t;
+            carry = t >> 32;
+        }
+    }
+    // R2: x = 2^(nbits-1) (< N), then 64L - nbits + 1 modular doublings
+    int top = L - 1;
+    while (top > 0 && n(top) == 0) top--;
+    const int nbits = 32 * top + (32 - __clz(n(top)));
+    for (int i = 0; i < L; i++) *wptr(X, count, k, i) = 0;
+    *wptr(X, count, k, (nbits - 1) >> 5) = 1u << ((nbits - 1) & 31);
+    const int steps = 64 * L - nbits + 1;
+    for (int s = 0; s < steps; s++) {
+        // x = 2x (with top bit out), then d = x - N; keep d if (out || no borrow)
+        uint32_t out = 0;
+        for (int i = 0; i < L; i++) {
+            uint32_t* xp = wptr(X, count, k, i);
+            const uint32_t v = *xp;
+            *xp = (v << 1) | out;
+            out = v >> 31;
+        }
+        uint32_t borrow = 0;
+        for (int i = 0; i < L; i++) {
+            const uint32_t v = *wptr(X, count, k, i), m = n(i);
+            const uint64_t d = (uint64_t)v - m - borrow;
+            *wptr(A, count, k, i) = (uint32_t)d;
+            borrow = (uint32_t)(d >> 63);
+        }
+        const uint32_t msk = 0u - ((out | (borrow ^ 1u)) & 1u);
+        for (int i = 0; i < L; i++) {
+            uint32_t* xp = wptr(X, count, k, i);
+            *xp = (*wptr(A, count, k, i) & msk) | (*xp & ~msk);
+        }
+    }
+    for (int i = 0; i < L; i++) *wptr(R2, count, k, i) = *wptr(X, count, k, i);
+}
+
+// ------------------------------------------------------------- dispatch
+// Compiled shapes: (C, NB) with L = C*NB.
+template <typename F>
+int dispatch_L(int L, F&& f) {
+    switch (L) {
+        case 16: return f(std::integral_constant<int, 16>{}, std::integral_constant<int, 1>{});
+        case 32: return f(std::integral_constant<int, 16>{}, std::integral_constant<int, 2>{});
+        case 64: return f(std::integral_constant<int, 16>{}, std::integral_constant<int, 4>{});
+        case 96: return f(std::integral_constant<int, 16>{}, std::integral_constant<int, 6>{});
+        case 128: return f(std::integral_constant<int, 16>{}, std::integral_constant<int, 8>{});
+        case 132: return f(std::integral_constant<int, 12>{}, std::integral_constant<int, 11>{});
+        default: return fail(MPB_EUNSUPPORTED, "unsupported limb count " + std::to_string(L));
+    }
+}
+
+bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+int check_ptrs(std::initializer_list<const void*> ps) {
+    for (const void* p : ps) {
+        if (!p) return fail(MPB_EINVAL, "null pointer");
+        if (!aligned16(p)) return fail(MPB_EINVAL, "pointer not 16-byte aligned");
+    }
+    return MPB_OK;
+}
+
+int check_launch() {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(MPB_ECUDA, std::string("CUDA launch failed: ") + cudaGetErrorString(e));
+    return MPB_OK;
+}
+
+unsigned grid_for(size_t n) { return (unsigned)((n + kThreads - 1) / kThreads); }
+
+int limbs_checked(int bits, int& L) {
+    L = mpb_limbs(bits);
+    if (L <= 0) return fail(MPB_EUNSUPPORTED, "bits must be positive");
+    switch (L) {
+        case 16: case 32: case 64: case 96: case 128: case 132: return MPB_OK;
+        default: return fail(MPB_EUNSUPPORTED, "bits=" + std::to_string(bits) + " not compiled (supported L: 16,32,64,96,128,132)");
+    }
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+int mpb_limbs(int bits) { return bits <= 0 ? 0 : 4 * ((bits + 127) / 128); }
+
+int mpb_supported(int bits) {
+    int L;
+    const std::string keep = g_err;
+    const int ok = limbs_checked(bits, L) == MPB_OK;
+    g_err = keep;
+    return ok;
+}
+
+const char* mpb_last_error(void) { return g_err.c_str(); }
+
+int mpb_layout_expand(const uint32_t* src, uint32_t* dst, size_t count, int limbs, void* stream) {
+    g_err.clear();
+    if (count == 0) return MPB_OK;
+    if (limbs <= 0 || limbs % 4) return fail(MPB_EINVAL, "limbs must be a positive multiple of 4");
+    if (int rc = check_ptrs({src, dst})) return rc;
+    if (src == dst) return fail(MPB_EINVAL, "in-place layout change not supported");
+    const size_t n = count * (size_t)(limbs / 4);
+    k_expand<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>((const uint4*)src, (uint4*)dst, count, limbs / 4);
+    return check_launch();
+}
+
+int mpb_layout_contract(const uint32_t* src, uint32_t* dst, size_t count, int limbs, void* stream) {
+    g_err.clear();
+    if (count == 0) return MPB_OK;
+    if (limbs <= 0 || limbs % 4) return fail(MPB_EINVAL, "limbs must be a positive multiple of 4");
+    if (int rc = check_ptrs({src, dst})) return rc;
+    if (src == dst) return fail(MPB_EINVAL, "in-place layout change not supported");
+    const size_t n = count * (size_t)(limbs / 4);
+    k_contract<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>((const uint4*)src, (uint4*)dst, count, limbs / 4);
+    return check_launch();
+}
+
+static int mp_product(const uint32_t* a, const uint32_t* b, uint32_t* c, size_t count, int bits, int algo, bool sqr,
+                      void* stream) {
+    g_err.clear();
+    if (algo < MPB_ALGO_AUTO || algo > MPB_ALGO_KARATSUBA) return fail(MPB_EINVAL, "algo out of range");
+    int L;
+    if (int rc = limbs_checked(bits, L)) return rc;
+    if (count == 0) return MPB_OK;
+    if (int rc = check_ptrs({a, b, c})) return rc;
+    if (c == a || c == b) return fail(MPB_EINVAL, "output aliases an input");
+    return dispatch_L(L, [&](auto Ci, auto NBi) {
+        constexpr int C = decltype(Ci)::value, NB = decltype(NBi)::value;
+        Launch<C, NB>::mp_mul(a, b, c, count, sqr, (cudaStream_t)stream);
+        return check_launch();
+    });
+}
+
+int mp_batch_mul(const uint32_t* a, const uint32_t* b, uint32_t* c, size_t count, int bits, int algo, void* stream) {
+    return mp_product(a, b, c, count, bits, algo, false, stream);
+}
+int mp_batch_sqr(const uint32_t* a, uint32_t* c, size_t count, int bits, int algo, void* stream) {
+    return mp_product(a, a, c, count, bits, algo, true, stream);
+}
+
+size_t mont_batch_workspace(size_t count, int bits) {
+    const int L = mpb_limbs(bits);
+    return count * (size_t)(3 * L) * sizeof(uint32_t);
+}
+
+static int mont_op(const uint32_t* a, const uint32_t* b, const uint32_t* N, const uint32_t* NP, uint32_t* c,
+                   size_t count, int bits, int redc, void* ws, size_t ws_bytes, bool sqr, void* stream) {
+    g_err.clear();
+    if (redc != MPB_REDC_FULL && redc != MPB_REDC_TRUNCATED) return fail(MPB_EINVAL, "redc out of range");
+    int L;
+    if (int rc = limbs_checked(bits, L)) return rc;
+    if (count == 0) return MPB_OK;
+    if (int rc = check_ptrs({a, b, N, NP, c, ws})) return rc;
+    if (c == a || c == b || c == N || c == NP) return fail(MPB_EINVAL, "output aliases an input");
+    if (ws_bytes < mont_batch_workspace(count, bits)) return fail(MPB_EINVAL, "workspace too small");
+    return dispatch_L(L, [&](auto Ci, auto NBi) {
+        constexpr int C = decltype(Ci)::value, NB = decltype(NBi)::value;
+        Launch<C, NB>::mont_mul(a, b, N, NP, c, count, redc == MPB_REDC_TRUNCATED, sqr, (uint32_t*)ws,
+                                (cudaStream_t)stream);
+        return check_launch();
+    });
+}
+
+int mont_batch_mul(const uint32_t* a, const uint32_t* b, const uint32_t* N, const uint32_t* NP, uint32_t* c,
+                   size_t count, int bits, int redc, void* ws, size_t ws_bytes, void* stream) {
+    return mont_op(a, b, N, NP, c, count, bits, redc, ws, ws_bytes, false, stream);
+}
+int mont_batch_sqr(const uint32_t* a, const uint32_t* N, const uint32_t* NP, uint32_t* c, size_t count, int bits,
+                   int redc, void* ws, size_t ws_bytes, void* stream) {
+    return mont_op(a, a, N, NP, c, count, bits, redc, ws, ws_bytes, true, stream);
+}
+
+int mont_batch_redc(const uint32_t* T, const uint32_t* N, const uint32_t* NP, uint32_t* c, size_t count, int bits,
+                    int redc, void* ws, size_t ws_bytes, void* stream) {
+    g_err.clear();
+    if (redc != MPB_REDC_FULL && redc != MPB_REDC_TRUNCATED) return fail(MPB_EINVAL, "redc out of range");
+    int L;
+    if (int rc = limbs_checked(bits, L)) return rc;
+    if (count == 0) return MPB_OK;
+    if (int rc = check_ptrs({T, N, NP, c, ws})) return rc;
+    if (c == T || c == N || c == NP) return fail(MPB_EINVAL, "output aliases an input");
+    if (ws_bytes < mont_batch_workspace(count, bits)) return fail(MPB_EINVAL, "workspace too small");
+    return dispatch_L(L, [&](auto Ci, auto NBi) {
+        constexpr int C = decltype(Ci)::value, NB = decltype(NBi)::value;
+        Launch<C, NB>::mont_redc(T, N, NP, c, count, redc == MPB_REDC_TRUNCATED, (uint32_t*)ws, (cudaStream_t)stream);
+        return check_launch();
+    });
+}
+
+size_t mont_batch_modexp_ct_workspace(size_t count, int bits, int window, int /*algo*/) {
+    const int L = mpb_limbs(bits);
+    if (window < 1 || window > 6) return 0;
+    return count * (size_t)L * (size_t)((1 << window) + 5) * sizeof(uint32_t);
+}
+
+int mont_batch_modexp_ct(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
+                         const uint32_t* exp, uint32_t* out, size_t count, int bits, int window, int redc, int algo,
+                         void* ws, size_t ws_bytes, void* stream) {
+    g_err.clear();
+    if (redc != MPB_REDC_FULL && redc != MPB_REDC_TRUNCATED) return fail(MPB_EINVAL, "redc out of range");
+    if (algo < MPB_ALGO_AUTO || algo > MPB_ALGO_KARATSUBA) return fail(MPB_EINVAL, "algo out of range");
+    if (window < 1 || window > 6) return fail(MPB_EINVAL, "window must be in 1..6");
+    int L;
+    if (int rc = limbs_checked(bits, L)) return rc;
+    if (count == 0) return MPB_OK;
+    if (int rc = check_ptrs({N, NP, R2, base, exp, out, ws})) return rc;
+    if (out == N || out == NP || out == R2 || out == base || out == exp)
+        return fail(MPB_EINVAL, "output aliases an input");
+    if (ws_bytes < mont_batch_modexp_ct_workspace(count, bits, window, algo))
+        return fail(MPB_EINVAL, "workspace too small");
+    return dispatch_L(L, [&](auto Ci, auto NBi) {
+        constexpr int C = decltype(Ci)::value, NB = decltype(NBi)::value;
+        Launch<C, NB>::modexp(N, NP, R2, base, exp, out, count, bits, window, redc == MPB_REDC_TRUNCATED,
+                              (uint32_t*)ws, (cudaStream_t)stream);
+        return check_launch();
+    });
+}
+
+size_t mont_batch_setup_workspace(size_t count, int bits) {
+    const int L = mpb_limbs(bits);
+    return count * (size_t)(2 * L + 4) * sizeof(uint32_t);
+}
+
+int mont_batch_setup(const uint32_t* N, uint32_t* NP, uint32_t* R2, size_t count, int bits, void* ws, size_t ws_bytes,
+                     void* stream) {
+    g_err.clear();
+    int L;
+    if (int rc = limbs_checked(bits, L)) return rc;
+    if (count == 0) return MPB_OK;
+    if (int rc = check_ptrs({N, NP, R2, ws})) return rc;
+    if (NP == N || R2 == N || NP == R2) return fail(MPB_EINVAL, "output aliases an input");
+    if (ws_bytes < mont_batch_setup_workspace(count, bits)) return fail(MPB_EINVAL, "workspace too small");
+    k_setup<<<grid_for(count), kThreads, 0, (cudaStream_t)stream>>>(N, NP, R2, count, L, (uint32_t*)ws);
+    return check_launch();
+}
+
+int mpb_modexp_host(const uint32_t* N, const uint32_t* base, const uint32_t* exp, uint32_t* out, size_t count,
+                    int bits, int window, int redc, void* stream) {
+    g_err.clear();
+    int L;
+    if (int rc = limbs_checked(bits, L)) return rc;
+    if (count == 0) return MPB_OK;
+    if (!N || !base || !exp || !out) return fail(MPB_EINVAL, "null pointer");
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t nb = count * (size_t)L * sizeof(uint32_t);
+    const size_t ws_bytes = mont_batch_modexp_ct_workspace(count, bits, window, 0);
+    const size_t setup_bytes = mont_batch_setup_workspace(count, bits);
+    uint8_t* dev = nullptr;
+    // 7 arrays of L limbs (N, N', R2, base, exp, out, staging) + workspace
+    const size_t total = 7 * nb + (ws_bytes > setup_bytes ? ws_bytes : setup_bytes) + 256;
+    if (cudaMallocAsync((void**)&dev, total, s) != cudaSuccess) return fail(MPB_ECUDA, "cudaMallocAsync failed");
+    uint32_t* d[7];
+    for (int i = 0; i < 7; i++) d[i] = (uint32_t*)(dev + i * nb);
+    void* ws = dev + 7 * nb;
+    const size_t wsz = total - 7 * nb;
+    int rc = MPB_OK;
+    auto h2d = [&](const uint32_t* h, uint32_t* dst) {
+        if (rc) return;
+        if (cudaMemcpyAsync(d[6], h, nb, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+            rc = fail(MPB_ECUDA, "H2D copy failed");
+            return;
+        }
+        rc = mpb_layout_expand(d[6], dst, count, L, stream);
+    };
+    h2d(N, d[0]);
+    h2d(base, d[3]);
+    h2d(exp, d[4]);
+    if (!rc) rc = mont_batch_setup(d[0], d[1], d[2], count, bits, ws, wsz, stream);
+    if (!rc) rc = mont_batch_modexp_ct(d[0], d[1], d[2], d[3], d[4], d[5], count, bits, window, redc, 0, ws, wsz, stream);
+    if (!rc) rc = mpb_layout_contract(d[5], d[6], count, L, stream);
+    if (!rc && cudaMemcpyAsync(out, d[6], nb, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        rc = fail(MPB_ECUDA, "D2H copy failed");
+    cudaFreeAsync(dev, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess && !rc) rc = fail(MPB_ECUDA, "stream sync failed");
+    return rc;
+}
+
+}  // extern "C"

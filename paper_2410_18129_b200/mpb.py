@@ -1,0 +1,215 @@
+"""Thin ctypes binding over libmpb.so (include/mpb.h).
+
+Argument marshalling only: every arithmetic step runs in the CUDA kernels of
+``csrc/``.  PyTorch provides device memory and the current stream.  There is
+no CPU fallback: importing this module without the built library, or calling
+it without a CUDA device, raises.
+
+Tensor conventions (all ``torch.int32`` holding uint32 bit patterns, on CUDA):
+  * operand-major:  shape (count, L)          -- operand k's limbs contiguous
+  * word-sliced:    shape (L // 4, count, 4)  -- the device layout of mpb.h
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmpb.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(there is no CPU fallback for the CUDA path)"
+    )
+
+_lib = ctypes.CDLL(LIB_PATH)
+_vp, _sz, _i = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
+_SIGS = {
+    "mpb_limbs": (_i, [_i]),
+    "mpb_supported": (_i, [_i]),
+    "mpb_layout_expand": (_i, [_vp, _vp, _sz, _i, _vp]),
+    "mpb_layout_contract": (_i, [_vp, _vp, _sz, _i, _vp]),
+    "mp_batch_mul": (_i, [_vp, _vp, _vp, _sz, _i, _i, _vp]),
+    "mp_batch_sqr": (_i, [_vp, _vp, _sz, _i, _i, _vp]),
+    "mont_batch_mul": (_i, [_vp, _vp, _vp, _vp, _vp, _sz, _i, _i, _vp, _sz, _vp]),
+    "mont_batch_sqr": (_i, [_vp, _vp, _vp, _vp, _sz, _i, _i, _vp, _sz, _vp]),
+    "mont_batch_redc": (_i, [_vp, _vp, _vp, _vp, _sz, _i, _i, _vp, _sz, _vp]),
+    "mont_batch_workspace": (_sz, [_sz, _i]),
+    "mont_batch_modexp_ct": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _sz, _i, _i, _i, _i, _vp, _sz, _vp]),
+    "mont_batch_modexp_ct_workspace": (_sz, [_sz, _i, _i, _i]),
+    "mont_batch_setup": (_i, [_vp, _vp, _vp, _sz, _i, _vp, _sz, _vp]),
+    "mont_batch_setup_workspace": (_sz, [_sz, _i]),
+    "mpb_modexp_host": (_i, [_vp, _vp, _vp, _vp, _sz, _i, _i, _i, _vp]),
+    "mpb_last_error": (ctypes.c_char_p, []),
+}
+for _name, (_res, _args) in _SIGS.items():
+    _f = getattr(_lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+
+MPB_OK, MPB_EINVAL, MPB_EUNSUPPORTED, MPB_ECUDA = 0, -1, -2, -3
+REDC_FULL, REDC_TRUNCATED = 0, 1
+ALGO_AUTO, ALGO_SCHOOLBOOK, ALGO_KARATSUBA = 0, 1, 2
+
+
+class MpbError(RuntimeError):
+    pass
+
+
+def _check(rc: int) -> None:
+    if rc == MPB_OK:
+        return
+    msg = _lib.mpb_last_error().decode()
+    if rc in (MPB_EINVAL, MPB_EUNSUPPORTED):
+        raise ValueError(f"mpb error {rc}: {msg}")
+    raise MpbError(f"mpb error {rc}: {msg}")
+
+
+def limbs(bits: int) -> int:
+    return _lib.mpb_limbs(bits)
+
+
+def supported(bits: int) -> bool:
+    return bool(_lib.mpb_supported(bits))
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("expected a CUDA tensor")
+    if t.dtype != torch.int32:
+        raise ValueError("expected torch.int32 (uint32 bit patterns)")
+    if not t.is_contiguous():
+        raise ValueError("expected a contiguous tensor")
+    return t.data_ptr()
+
+
+def _sliced_shape(t: torch.Tensor) -> tuple[int, int]:
+    if t.dim() != 3 or t.shape[2] != 4:
+        raise ValueError("word-sliced tensors have shape (L//4, count, 4)")
+    return 4 * t.shape[0], t.shape[1]
+
+
+def empty_sliced(L: int, count: int, device="cuda") -> torch.Tensor:
+    return torch.empty((L // 4, count, 4), dtype=torch.int32, device=device)
+
+
+def workspace(nbytes: int, device="cuda") -> torch.Tensor:
+    return torch.empty((max(16, nbytes) + 15) // 16 * 4, dtype=torch.int32, device=device)
+
+
+# ------------------------------------------------------------------- layout
+def layout_expand(x: torch.Tensor) -> torch.Tensor:
+    """operand-major (count, L) -> word-sliced (L//4, count, 4)  (the paper's `expand`)."""
+    count, L = x.shape
+    out = empty_sliced(L, count, x.device)
+    _check(_lib.mpb_layout_expand(_ptr(x), _ptr(out), count, L, _stream()))
+    return out
+
+
+def layout_contract(y: torch.Tensor) -> torch.Tensor:
+    """word-sliced (L//4, count, 4) -> operand-major (count, L)  (the paper's `contract`)."""
+    L, count = _sliced_shape(y)
+    out = torch.empty((count, L), dtype=torch.int32, device=y.device)
+    _check(_lib.mpb_layout_contract(_ptr(y), _ptr(out), count, L, _stream()))
+    return out
+
+
+# --------------------------------------------------------------- products
+def mp_batch_mul(a: torch.Tensor, b: torch.Tensor, bits: int, algo: int = ALGO_AUTO) -> torch.Tensor:
+    L, count = _sliced_shape(a)
+    c = empty_sliced(2 * L, count, a.device)
+    _check(_lib.mp_batch_mul(_ptr(a), _ptr(b), _ptr(c), count, bits, algo, _stream()))
+    return c
+
+
+def mp_batch_sqr(a: torch.Tensor, bits: int, algo: int = ALGO_AUTO) -> torch.Tensor:
+    L, count = _sliced_shape(a)
+    c = empty_sliced(2 * L, count, a.device)
+    _check(_lib.mp_batch_sqr(_ptr(a), _ptr(c), count, bits, algo, _stream()))
+    return c
+
+
+def mont_workspace(count: int, bits: int, device="cuda") -> torch.Tensor:
+    return workspace(_lib.mont_batch_workspace(count, bits), device)
+
+
+def mont_batch_mul(a, b, N, Np, bits: int, redc: int = REDC_TRUNCATED, ws: torch.Tensor | None = None):
+    L, count = _sliced_shape(a)
+    ws = ws if ws is not None else mont_workspace(count, bits, a.device)
+    c = empty_sliced(L, count, a.device)
+    _check(_lib.mont_batch_mul(_ptr(a), _ptr(b), _ptr(N), _ptr(Np), _ptr(c), count, bits, redc, _ptr(ws),
+                               ws.numel() * 4, _stream()))
+    return c
+
+
+def mont_batch_sqr(a, N, Np, bits: int, redc: int = REDC_TRUNCATED, ws: torch.Tensor | None = None):
+    L, count = _sliced_shape(a)
+    ws = ws if ws is not None else mont_workspace(count, bits, a.device)
+    c = empty_sliced(L, count, a.device)
+    _check(_lib.mont_batch_sqr(_ptr(a), _ptr(N), _ptr(Np), _ptr(c), count, bits, redc, _ptr(ws), ws.numel() * 4,
+                               _stream()))
+    return c
+
+
+def mont_batch_redc(T, N, Np, bits: int, redc: int = REDC_TRUNCATED, ws: torch.Tensor | None = None):
+    L, count = _sliced_shape(N)
+    ws = ws if ws is not None else mont_workspace(count, bits, N.device)
+    c = empty_sliced(L, count, N.device)
+    _check(_lib.mont_batch_redc(_ptr(T), _ptr(N), _ptr(Np), _ptr(c), count, bits, redc, _ptr(ws), ws.numel() * 4,
+                                _stream()))
+    return c
+
+
+def mont_batch_setup(N: torch.Tensor, bits: int) -> tuple[torch.Tensor, torch.Tensor]:
+    L, count = _sliced_shape(N)
+    Np, R2 = empty_sliced(L, count, N.device), empty_sliced(L, count, N.device)
+    ws = workspace(_lib.mont_batch_setup_workspace(count, bits), N.device)
+    _check(_lib.mont_batch_setup(_ptr(N), _ptr(Np), _ptr(R2), count, bits, _ptr(ws), ws.numel() * 4, _stream()))
+    return Np, R2
+
+
+def modexp_workspace(count: int, bits: int, window: int, algo: int = ALGO_AUTO, device="cuda") -> torch.Tensor:
+    return workspace(_lib.mont_batch_modexp_ct_workspace(count, bits, window, algo), device)
+
+
+def mont_batch_modexp_ct(N, Np, R2, base, exp, bits: int, window: int = 5, redc: int = REDC_TRUNCATED,
+                         algo: int = ALGO_AUTO, ws: torch.Tensor | None = None, out: torch.Tensor | None = None):
+    L, count = _sliced_shape(N)
+    ws = ws if ws is not None else modexp_workspace(count, bits, window, algo, N.device)
+    out = out if out is not None else empty_sliced(L, count, N.device)
+    _check(_lib.mont_batch_modexp_ct(_ptr(N), _ptr(Np), _ptr(R2), _ptr(base), _ptr(exp), _ptr(out), count, bits,
+                                     window, redc, algo, _ptr(ws), ws.numel() * 4, _stream()))
+    return out
+
+
+def modexp_host(N: np.ndarray, base: np.ndarray, exp: np.ndarray, bits: int, window: int = 5,
+                redc: int = REDC_TRUNCATED) -> np.ndarray:
+    """End-to-end over host buffers (operand-major uint32 (count, L)); blocking."""
+    N, base, exp = (np.ascontiguousarray(x, dtype=np.uint32) for x in (N, base, exp))
+    count, L = N.shape
+    out = np.empty_like(N)
+    _check(_lib.mpb_modexp_host(N.ctypes.data, base.ctypes.data, exp.ctypes.data, out.ctypes.data, count, bits,
+                                window, redc, _stream()))
+    return out
+
+
+# ------------------------------------------------------- host <-> device
+def to_device(x: np.ndarray, device="cuda") -> torch.Tensor:
+    """operand-major uint32 numpy (count, L) -> word-sliced CUDA tensor."""
+    t = torch.from_numpy(np.ascontiguousarray(x, dtype=np.uint32).view(np.int32)).to(device)
+    return layout_expand(t)
+
+
+def to_host(y: torch.Tensor) -> np.ndarray:
+    """word-sliced CUDA tensor -> operand-major uint32 numpy (count, L)."""
+    return layout_contract(y).cpu().numpy().view(np.uint32)

@@ -1,0 +1,79 @@
+"""CPU-side checks of the boundary: the C-ABI library loads and exports every symbol that
+include/mpb.h declares (no compute calls -- there is no GPU here), host-only helpers
+behave, and the product path never reaches the oracle."""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "mpb.h")
+LIB = os.path.join(ROOT, "paper_2410_18129_b200", "libmpb.so")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"^\s*(?:const\s+)?[A-Za-z_][A-Za-z0-9_]*\s*\**\s*([a-z_][a-z0-9_]*)\s*\(", src, flags=re.M)
+    return sorted(set(names))
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for required in ["mp_batch_mul", "mp_batch_sqr", "mont_batch_mul", "mont_batch_sqr", "mont_batch_redc",
+                     "mont_batch_modexp_ct", "mont_batch_setup", "mpb_layout_expand", "mpb_layout_contract",
+                     "mpb_last_error"]:
+        assert required in names
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(LIB):
+        import __graft_entry__ as g
+
+        g.build_cuda()
+    return ctypes.CDLL(LIB)
+
+
+def test_library_exports_every_declared_symbol(lib):
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_host_only_helpers(lib):
+    lib.mpb_limbs.restype = ctypes.c_int
+    lib.mpb_supported.restype = ctypes.c_int
+    assert [lib.mpb_limbs(b) for b in (0, 1, 512, 1024, 2048, 3072, 4096, 4108, 4154)] == \
+        [0, 4, 16, 32, 64, 96, 128, 132, 132]
+    assert lib.mpb_supported(2048) == 1 and lib.mpb_supported(700) == 0
+    lib.mont_batch_modexp_ct_workspace.restype = ctypes.c_size_t
+    lib.mont_batch_modexp_ct_workspace.argtypes = [ctypes.c_size_t, ctypes.c_int, ctypes.c_int, ctypes.c_int]
+    assert lib.mont_batch_modexp_ct_workspace(10, 2048, 5, 0) == 10 * 64 * (32 + 5) * 4
+    assert lib.mont_batch_modexp_ct_workspace(10, 2048, 7, 0) == 0
+
+
+def test_product_path_never_imports_the_oracle():
+    pkg = os.path.join(ROOT, "paper_2410_18129_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(import|from)\s+oracle\b", txt, flags=re.M), f
+                assert "oracle.h" not in txt, f
+
+
+def test_binding_fails_loudly_without_library(tmp_path, monkeypatch):
+    """The binding has no CPU fallback: with the .so absent, import raises."""
+    import importlib.util
+
+    src = os.path.join(ROOT, "paper_2410_18129_b200", "mpb.py")
+    fake_pkg = tmp_path / "fakepkg"
+    fake_pkg.mkdir()
+    (fake_pkg / "mpb.py").write_text(open(src).read())
+    spec = importlib.util.spec_from_file_location("fakepkg_mpb", fake_pkg / "mpb.py")
+    mod = importlib.util.module_from_spec(spec)
+    with pytest.raises(ImportError):
+        spec.loader.exec_module(mod)

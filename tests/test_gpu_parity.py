@@ -1,0 +1,250 @@
+"""GPU parity: every C-ABI entry point of libmpb.so against the CPU oracle, bit-exact.
+
+All arithmetic is exact unsigned integer ("no floating point, no rounding
+and no tolerance anywhere on this path"), so every comparison is element-by-element
+equality.  Sizes span several C=16-limb blocks and ragged batch tails (count not a
+multiple of the 128-thread CTA); the full-size cases sample outputs the oracle can
+recompute one by one and check truncated == full REDC on the whole batch.
+"""
+from __future__ import annotations
+
+import random
+
+import numpy as np
+import pytest
+
+import oracle as O
+from adversarial import redc_family
+from paper_2410_18129_b200 import inputs as I
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+BITS_MOD = [512, 1024, 2048, 3072, 4096, 4108]
+BITS_MUL = [512, 1024, 2048, 3072, 4096, 4154]
+REDC = [1, 0]  # truncated, full
+
+
+@pytest.fixture(scope="module")
+def mpb():
+    from paper_2410_18129_b200 import mpb as m
+
+    return m
+
+
+def ints(arr):
+    return I.array_to_ints(arr)
+
+
+def structured_operands(N_ints, L):
+    """Edge operands below each modulus: 0, 1, N-1, 2^k, all-ones below N, N>>1."""
+    out = []
+    for n in N_ints:
+        cands = [0, 1, n - 1, n >> 1, (1 << (n.bit_length() - 1)) - 1, 1 << (n.bit_length() // 2)]
+        out.append(cands)
+    return out
+
+
+# ------------------------------------------------------------------------ layout
+@pytest.mark.parametrize("L,count", [(4, 1), (16, 33), (64, 1000), (132, 129)])
+def test_layout_roundtrip(mpb, L, count):
+    rng = np.random.default_rng(L * 1000 + count)
+    x = rng.integers(0, 1 << 32, size=(count, L), dtype=np.uint64).astype(np.uint32)
+    d = mpb.to_device(x)
+    assert d.shape == (L // 4, count, 4)
+    # the device layout is exactly the documented word-sliced formula
+    flat = d.cpu().numpy().view(np.uint32).reshape(-1)
+    for (k, i) in [(0, 0), (count - 1, L - 1), (count // 2, L // 2)]:
+        assert flat[((i // 4) * count + k) * 4 + (i % 4)] == x[k, i]
+    assert np.array_equal(mpb.to_host(d), x)
+
+
+# ---------------------------------------------------------------------- products
+@pytest.mark.parametrize("bits", BITS_MUL)
+def test_mp_batch_mul_sqr(mpb, bits):
+    count = 130  # ragged over 128-thread CTAs
+    a, b = I.mul_inputs(config=4, count=count, bits=bits)
+    L = a.shape[1]
+    # structured rows: all ones (carry worst case), zero, one, powers of two
+    a[0] = np.uint32(0xFFFFFFFF); b[0] = np.uint32(0xFFFFFFFF)
+    a[1] = 0; a[2] = 0; a[2, 0] = 1
+    a[3] = 0; a[3, L - 1] = np.uint32(1 << 31); b[3] = np.uint32(0xFFFFFFFF)
+    da, db = mpb.to_device(a), mpb.to_device(b)
+    c = mpb.to_host(mpb.mp_batch_mul(da, db, bits))
+    s = mpb.to_host(mpb.mp_batch_sqr(da, bits))
+    A, B = ints(a), ints(b)
+    for k in range(count):
+        assert I.from_limbs(c[k]) == O.mul(A[k], B[k]), k
+        assert I.from_limbs(s[k]) == O.sqr(A[k]), k
+
+
+# ------------------------------------------------------------------------- setup
+@pytest.mark.parametrize("bits", BITS_MOD)
+def test_setup(mpb, bits):
+    count = 40
+    N, _, _ = I.modexp_inputs(config=2, count=count, bits=bits)
+    L = N.shape[1]
+    Np, R2 = mpb.mont_batch_setup(mpb.to_device(N), bits)
+    Np, R2 = mpb.to_host(Np), mpb.to_host(R2)
+    for k, n in enumerate(ints(N)):
+        np_ref, r2_ref = O.setup(n, L)
+        assert I.from_limbs(Np[k]) == np_ref
+        assert I.from_limbs(R2[k]) == r2_ref
+
+
+def _mont_fixture(mpb, bits, count, config=2):
+    N, a, b = I.montmul_inputs(config=config, count=count, bits=bits)
+    dN = mpb.to_device(N)
+    Np, R2 = mpb.mont_batch_setup(dN, bits)
+    return N, a, b, dN, Np, R2
+
+
+# ----------------------------------------------------------- montmul / montsqr
+@pytest.mark.parametrize("redc", REDC)
+@pytest.mark.parametrize("bits", BITS_MOD)
+def test_mont_mul_sqr(mpb, bits, redc):
+    count = 131
+    N, a, b, dN, Np, R2 = _mont_fixture(mpb, bits, count)
+    L = N.shape[1]
+    # edge operands in the first rows
+    for k, n in enumerate(ints(N[:6])):
+        ev = [0, 1, n - 1, n >> 1, n - 2, (n - 1) // 3][k]
+        a[k] = I.to_limbs(ev, L)
+        b[k] = I.to_limbs([n - 1, n - 1, n - 1, 1, n - 2, 0][k], L)
+    da, db = mpb.to_device(a), mpb.to_device(b)
+    c = mpb.to_host(mpb.mont_batch_mul(da, db, dN, Np, bits, redc=redc))
+    s = mpb.to_host(mpb.mont_batch_sqr(da, dN, Np, bits, redc=redc))
+    ref_c = O.batch_montmul(a, b, N)
+    ref_s = O.batch_montmul(a, a, N)
+    assert np.array_equal(c, ref_c)
+    assert np.array_equal(s, ref_s)
+
+
+# --------------------------------------------------------------------- REDC
+@pytest.mark.parametrize("redc", REDC)
+@pytest.mark.parametrize("bits", BITS_MOD)
+def test_mont_redc_adversarial(mpb, bits, redc):
+    """The exact carry correction of Theorem 2 (families alpha..delta, tests/adversarial.py)."""
+    L = I.limbs_for_bits(bits)
+    rng = random.Random(bits * 7 + redc)
+    N_arr, _, _ = I.modexp_inputs(config=1, count=6, bits=bits)
+    Ts, Ns = [], []
+    for n in ints(N_arr):
+        R = 1 << (32 * L)
+        for fam, t in redc_family(rng, n, L, per_family=4) + [("random", rng.randrange(n * R))]:
+            Ts.append(t)
+            Ns.append(n)
+    count = len(Ts)
+    T = I.ints_to_array(Ts, 2 * L)
+    N = I.ints_to_array(Ns, L)
+    dN = mpb.to_device(N)
+    Np, _ = mpb.mont_batch_setup(dN, bits)
+    c = mpb.to_host(mpb.mont_batch_redc(mpb.to_device(T), dN, Np, bits, redc=redc))
+    for k in range(count):
+        assert I.from_limbs(c[k]) == O.redc(Ts[k], Ns[k], L), k
+
+
+# ------------------------------------------------------------------- modexp
+MODEXP_COUNTS = {512: 70, 1024: 40, 2048: 10, 3072: 4, 4096: 3, 4108: 3}
+
+
+@pytest.mark.parametrize("redc", REDC)
+@pytest.mark.parametrize("bits", BITS_MOD)
+def test_modexp(mpb, bits, redc):
+    count = MODEXP_COUNTS[bits]
+    N, base, exp = I.modexp_inputs(config=3, count=count, bits=bits)
+    dN = mpb.to_device(N)
+    Np, R2 = mpb.mont_batch_setup(dN, bits)
+    out = mpb.to_host(mpb.mont_batch_modexp_ct(dN, Np, R2, mpb.to_device(base), mpb.to_device(exp), bits,
+                                               window=5, redc=redc))
+    ref = O.batch_modexp(base, exp, bits, N)
+    assert np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("window", [1, 2, 3, 4, 5, 6])
+def test_modexp_window_independence(mpb, window):
+    bits, count = 1024, 20
+    N, base, exp = I.modexp_inputs(config=1, count=count, bits=bits)
+    dN = mpb.to_device(N)
+    Np, R2 = mpb.mont_batch_setup(dN, bits)
+    out = mpb.to_host(mpb.mont_batch_modexp_ct(dN, Np, R2, mpb.to_device(base), mpb.to_device(exp), bits,
+                                               window=window))
+    assert np.array_equal(out, O.batch_modexp(base, exp, bits, N))
+
+
+def test_modexp_special_exponents_and_bases(mpb):
+    bits = 1024
+    L = I.limbs_for_bits(bits)
+    N, base, exp = I.modexp_inputs(config=1, count=12, bits=bits)
+    Ns = ints(N)
+    cases = [(0, 0), (5, 0), (0, 7), (1, (1 << bits) - 1), (Ns[4] - 1, 1234), (Ns[5] - 1, 1235),
+             (3, 1), (3, 2), (7, (1 << bits) - 1), (11, 1 << (bits - 1)), (2, 31), (Ns[11] - 2, 5)]
+    for k, (bv, ev) in enumerate(cases):
+        base[k] = I.to_limbs(bv, L)
+        exp[k] = I.to_limbs(ev, L)
+    dN = mpb.to_device(N)
+    Np, R2 = mpb.mont_batch_setup(dN, bits)
+    out = mpb.to_host(mpb.mont_batch_modexp_ct(dN, Np, R2, mpb.to_device(base), mpb.to_device(exp), bits))
+    for k, (bv, ev) in enumerate(cases):
+        assert I.from_limbs(out[k]) == O.modexp(bv, ev, Ns[k], L, ebits=bits), k
+
+
+def test_modexp_fermat_primes(mpb):
+    """a^(p-1) = 1 mod p for Miller-Rabin primes from the oracle (north_star Fermat pin)."""
+    bits = 512
+    L = I.limbs_for_bits(bits)
+    ps = [O.gen_prime(bits, seed=100 + i) for i in range(4)]
+    rng = random.Random(5)
+    N = I.ints_to_array(ps, L)
+    base = I.ints_to_array([rng.randrange(2, p - 1) for p in ps], L)
+    exp = I.ints_to_array([p - 1 for p in ps], L)
+    dN = mpb.to_device(N)
+    Np, R2 = mpb.mont_batch_setup(dN, bits)
+    out = mpb.to_host(mpb.mont_batch_modexp_ct(dN, Np, R2, mpb.to_device(base), mpb.to_device(exp), bits))
+    assert all(I.from_limbs(r) == 1 for r in out)
+
+
+def test_modexp_host_e2e(mpb):
+    bits, count = 1024, 9
+    N, base, exp = I.modexp_inputs(config=5, count=count, bits=bits)
+    out = mpb.modexp_host(N, base, exp, bits, window=5)
+    assert np.array_equal(out, O.batch_modexp(base, exp, bits, N))
+
+
+# -------------------------------------------------- full-size, sampled checks
+@pytest.mark.slow
+def test_config3_full_batch_sampled(mpb):
+    """Config 3 at its full size (2048-bit, 2^18, w=5), in the launch configuration bench.py times:
+    a seeded sample of outputs against the oracle, and truncated == full on the whole batch."""
+    bits, count = 2048, 1 << 18
+    N, base, exp = I.modexp_inputs(config=3, count=count, bits=bits)
+    dN, dB, dE = (mpb.to_device(x) for x in (N, base, exp))
+    Np, R2 = mpb.mont_batch_setup(dN, bits)
+    ws = mpb.modexp_workspace(count, bits, 5)
+    out_t = mpb.mont_batch_modexp_ct(dN, Np, R2, dB, dE, bits, 5, redc=1, ws=ws)
+    out_f = mpb.mont_batch_modexp_ct(dN, Np, R2, dB, dE, bits, 5, redc=0, ws=ws)
+    assert torch.equal(out_t, out_f)
+    h = mpb.to_host(out_t)
+    idx = np.random.default_rng(3).choice(count, size=48, replace=False)
+    idx = np.concatenate([idx, [0, count - 1]])
+    ref = O.batch_modexp(base[idx], exp[idx], bits, N[idx])
+    assert np.array_equal(h[idx], ref)
+
+
+# ------------------------------------------------------------- ABI errors
+def test_abi_errors_and_noop(mpb):
+    bits = 1024
+    N, a, b = I.montmul_inputs(config=2, count=4, bits=bits)
+    dN, da = mpb.to_device(N), mpb.to_device(a)
+    Np, R2 = mpb.mont_batch_setup(dN, bits)
+    with pytest.raises(ValueError):
+        mpb.mont_batch_modexp_ct(dN, Np, R2, da, da, bits, window=7)
+    with pytest.raises(ValueError):
+        mpb.mont_batch_mul(da, da, dN, Np, bits, redc=5)
+    with pytest.raises(ValueError):
+        mpb.mp_batch_mul(da, da, 700)  # L = 24 not compiled
+    assert not mpb.supported(700) and mpb.supported(2048) and mpb.supported(4108)
+    # count == 0 is a no-op
+    z = mpb.empty_sliced(32, 0)
+    assert mpb.mp_batch_mul(z, z, bits).shape == (16, 0, 4)
