@@ -15,9 +15,8 @@ constexpr int kThreads = 128;
 
 MPB_DEVI size_t tid_global() { return (size_t)blockIdx.x * blockDim.x + threadIdx.x; }
 // word-sliced accessor for operand k of an array with `count` operands
-MPB_DEVI GArr garr(uint32_t* base, size_t count, size_t k) { return GArr{reinterpret_cast<uint4*>(base) + k, count}; }
-MPB_DEVI GIn gin(const uint32_t* base, size_t count, size_t k) {
-    return GIn{reinterpret_cast<const uint4*>(base) + k, count};
+MPB_DEVI Arr arr(const uint32_t* base, size_t count, size_t k) {
+    return Arr{reinterpret_cast<uint4*>(const_cast<uint32_t*>(base)) + k, count};
 }
 // word i of operand k (32-bit access)
 MPB_DEVI uint32_t word_at(const uint32_t* base, size_t count, size_t k, int i) {
@@ -30,7 +29,10 @@ __global__ void __launch_bounds__(kThreads) k_mp_mul(const uint32_t* __restrict_
                                                      uint32_t* __restrict__ c, size_t count) {
     const size_t k = tid_global();
     if (k >= count) return;
-    ph_product<C, NB, SQR>(gin(a, count, k), gin(SQR ? a : b, count, k), garr(c, count, k));
+    uint32_t orlo = 0, tl1 = 0;
+    const Arr C_ = arr(c, count, k);
+    engine<C, NB, true>(SQR ? PH_SQR : PH_MUL, arr(a, count, k), arr(SQR ? a : b, count, k), C_, C_, C_, C_, orlo,
+                        tl1);
 }
 
 // workspace for the mont kernels: T (2L) then Q (L), word-sliced with stride count
@@ -41,10 +43,9 @@ __global__ void __launch_bounds__(kThreads) k_mont_mul(const uint32_t* __restric
     constexpr int L = C * NB;
     const size_t k = tid_global();
     if (k >= count) return;
-    const GArr T = garr(ws, count, k);
-    const GArr Q = garr(ws + (size_t)2 * L * count, count, k);
-    mont_mul<C, NB, TRUNC, SQR>(gin(a, count, k), gin(SQR ? a : b, count, k), gin(N, count, k), gin(NP, count, k), T,
-                                Q, garr(c, count, k));
+    const Arr T = arr(ws, count, k), Q = arr(ws + (size_t)2 * L * count, count, k);
+    mont_op<C, NB, TRUNC>(SQR ? MODE_SQR : MODE_MUL, arr(a, count, k), arr(SQR ? a : b, count, k), arr(N, count, k),
+                          arr(NP, count, k), T, Q, arr(c, count, k));
 }
 
 template <int C, int NB, bool TRUNC>
@@ -54,77 +55,94 @@ __global__ void __launch_bounds__(kThreads) k_mont_redc(const uint32_t* __restri
     constexpr int L = C * NB;
     const size_t k = tid_global();
     if (k >= count) return;
-    const GArr T = garr(ws, count, k);
-    const GArr Q = garr(ws + (size_t)2 * L * count, count, k);
-    const GIn Ti = gin(Tin, count, k);
+    const Arr T = arr(ws, count, k), Q = arr(ws + (size_t)2 * L * count, count, k);
+    const Arr Ti = arr(Tin, count, k);
 #pragma unroll 1
     for (int q = 0; q < 2 * L / 4; q++) T.st(q, Ti.ld(q));
-    mont_redc<C, NB, TRUNC>(gin(N, count, k), gin(NP, count, k), T, Q, garr(c, count, k));
+    mont_op<C, NB, TRUNC>(MODE_REDC, T, T, arr(N, count, k), arr(NP, count, k), T, Q, arr(c, count, k));
 }
 
 // ------------------------------------------------------------------- modexp
+// alg:8FWExp as one flat, public schedule of operations so that the kernel
+// holds a single instance of the Montgomery engine:
+//   op 0             G[0] = REDC(R^2) = R mod N               (Montgomery one)
+//   op 1             G[1] = MontMul(base, R^2)
+//   op e < 2^w       G[e] = MontMul(G[e-1], G[1])
+//   op 2^w           Y = CTsel(G, top window)                  (windows LSB-aligned, A11)
+//   then per window j = W-2 .. 0:  w x Y = MontSqr(Y),  S = CTsel(G, window j)
+//                                  (P:L765-766),  Y = MontMul(Y, S)
+//   last op          out = REDC(Y)
 // workspace per operand (word-sliced, stride count): G (2^w * L) | Y (L) | T (2L) | Q (L) | S (L)
 template <int C, int NB, bool TRUNC>
 __global__ void __launch_bounds__(kThreads) k_modexp(const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP,
                                                      const uint32_t* __restrict__ R2, const uint32_t* __restrict__ base,
                                                      const uint32_t* __restrict__ exp, uint32_t* __restrict__ out,
                                                      size_t count, int bits, int w, uint32_t* ws) {
-    constexpr int L = C * NB;
+    constexpr int L = C * NB, Q4 = L / 4;
     const size_t k = tid_global();
     if (k >= count) return;
     const int nent = 1 << w;
     uint32_t* p = ws;
-    const GArr G = garr(p, count, k);
+    const Arr G = arr(p, count, k);
     p += (size_t)nent * L * count;
-    const GArr Y = garr(p, count, k);
+    const Arr Y = arr(p, count, k);
     p += (size_t)L * count;
-    const GArr T = garr(p, count, k);
+    const Arr T = arr(p, count, k);
     p += (size_t)2 * L * count;
-    const GArr Q = garr(p, count, k);
+    const Arr Q = arr(p, count, k);
     p += (size_t)L * count;
-    const GArr S = garr(p, count, k);
-    const GIn Nn = gin(N, count, k), NPn = gin(NP, count, k), R2n = gin(R2, count, k), Bn = gin(base, count, k);
-    auto Gent = [&](int e) { return GArr{G.p + (size_t)e * (L / 4) * count, count}; };
+    const Arr S = arr(p, count, k);
+    const Arr Nn = arr(N, count, k), NPn = arr(NP, count, k), R2n = arr(R2, count, k), Bn = arr(base, count, k);
+    const Arr On = arr(out, count, k);
 
-    // G[0] = R mod N = REDC(R^2)  (Montgomery one, SURVEY A11 "1 = R mod N")
-#pragma unroll 1
-    for (int q = 0; q < L / 4; q++) {
-        T.st(q, R2n.ld(q));
-        T.st(L / 4 + q, make_uint4(0, 0, 0, 0));
-    }
-    mont_redc<C, NB, TRUNC>(Nn, NPn, T, Q, Gent(0));
-    // G[1] = base * R mod N = MontMul(base, R^2);  G[i] = MontMul(G[i-1], G[1])
-    if (nent > 1) mont_mul<C, NB, TRUNC, false>(Bn, R2n, Nn, NPn, T, Q, Gent(1));
-#pragma unroll 1
-    for (int e = 2; e < nent; e++) mont_mul<C, NB, TRUNC, false>(Gent(e - 1), Gent(1), Nn, NPn, T, Q, Gent(e));
-
-    // windows are LSB-aligned: window j covers exponent bits [j*w, j*w + w)
     const int nwin = (bits + w - 1) / w;
-    auto window = [&](int j) -> uint32_t {
-        const int pos = j * w;
-        const int wi = pos >> 5, off = pos & 31;
-        uint32_t v = word_at(exp, count, k, wi) >> off;
-        if (off + w > 32 && wi + 1 < L) v |= word_at(exp, count, k, wi + 1) << (32 - off);
-        return v & ((1u << w) - 1u);
-    };
-    // Y = G[top window] (the top partial window initialises Y; no epilogue)
-    ct_select<L>(G, nent, window(nwin - 1), Y);
+    const int per_win = w + 2;
+    const int n_ops = nent + 1 + (nwin - 1) * per_win + 1;
 #pragma unroll 1
-    for (int j = nwin - 2; j >= 0; j--) {
+    for (int op = 0; op < n_ops; op++) {
+        int mode = MODE_MUL;
+        bool select = false;
+        int win = 0;
+        Arr X = Y, B = Y, O = Y;
+        if (op == 0) {
+            mode = MODE_REDC; X = R2n; O = G;
+        } else if (op < nent) {
+            X = op == 1 ? Bn : G.at((op - 1) * Q4);
+            B = op == 1 ? R2n : G.at(Q4);
+            O = G.at(op * Q4);
+        } else if (op == nent) {
+            select = true; win = nwin - 1; O = Y;
+        } else if (op == n_ops - 1) {
+            mode = MODE_REDC; X = Y; O = On;
+        } else {
+            const int r = (op - nent - 1) % per_win;
+            win = nwin - 2 - (op - nent - 1) / per_win;
+            if (r < w) {
+                mode = MODE_SQR;
+            } else if (r == w) {
+                select = true; O = S;
+            } else {
+                B = S;
+            }
+        }
+        if (select) {
+            // w bits of the exponent at public position win*w (may straddle two words)
+            const int pos = win * w, wi = pos >> 5, off = pos & 31;
+            uint32_t v = word_at(exp, count, k, wi) >> off;
+            if (off + w > 32 && wi + 1 < L) v |= word_at(exp, count, k, wi + 1) << (32 - off);
+            ct_select<L>(G, nent, v & ((1u << w) - 1u), O);
+            continue;
+        }
+        if (mode == MODE_REDC) {  // T = X zero-extended to 2L limbs
 #pragma unroll 1
-        for (int s = 0; s < w; s++) mont_mul<C, NB, TRUNC, true>(Y, Y, Nn, NPn, T, Q, Y);
-        ct_select<L>(G, nent, window(j), S);
-        mont_mul<C, NB, TRUNC, false>(Y, S, Nn, NPn, T, Q, Y);
+            for (int q = 0; q < Q4; q++) {
+                T.st(q, X.ld(q));
+                T.st(Q4 + q, make_uint4(0, 0, 0, 0));
+            }
+        }
+        mont_op<C, NB, TRUNC>(mode, X, B, Nn, NPn, T, Q, O);
     }
-    // leave the Montgomery domain: out = REDC(Y)
-#pragma unroll 1
-    for (int q = 0; q < L / 4; q++) {
-        T.st(q, Y.ld(q));
-        T.st(L / 4 + q, make_uint4(0, 0, 0, 0));
-    }
-    mont_redc<C, NB, TRUNC>(Nn, NPn, T, Q, garr(out, count, k));
 }
-
 
 inline unsigned grid_for(size_t n) { return (unsigned)((n + kThreads - 1) / kThreads); }
 

@@ -168,7 +168,7 @@ MPB_DEVI void bp_sqr_offdiag(const uint32_t (&x)[C], uint32_t (&E)[2 * C], uint3
 
 // Low half: value = E[0..C) + O[0..C-1)*2^32 == x*y (mod 2^{32C}); the top column is lo-only.
 template <int C>
-MPB_DEVI void bp_lo(const uint32_t (&x)[C], const uint32_t (&y)[C], uint32_t (&E)[C], uint32_t (&O)[C]) {
+MPB_DEVI void bp_lo(const uint32_t (&x)[C], const uint32_t (&y)[C], uint32_t (&E)[2 * C], uint32_t (&O)[2 * C]) {
     static_assert(C % 2 == 0, "even block");
 #pragma unroll
     for (int j = 0; j < C - 1; j++) {  // row 0 fresh (positions j)
@@ -204,7 +204,7 @@ MPB_DEVI void bp_lo(const uint32_t (&x)[C], const uint32_t (&y)[C], uint32_t (&E
 //   R = sum_{i+j>=C-1} x_i y_j 2^{32(i+j-C+1)} + sum_{i+j=C-2} hi(x_i y_j)
 // value = E[0..C+1) + O[1..C+2)*2^0  with O[k] at relative position k-1 (O[0] is a dummy lo word).
 template <int C>
-MPB_DEVI void bp_hi(const uint32_t (&x)[C], const uint32_t (&y)[C], uint32_t (&E)[C + 2], uint32_t (&O)[C + 2]) {
+MPB_DEVI void bp_hi(const uint32_t (&x)[C], const uint32_t (&y)[C], uint32_t (&E)[2 * C], uint32_t (&O)[2 * C]) {
     static_assert(C % 2 == 0 && C >= 4, "even block >= 4");
 #pragma unroll
     for (int k = 0; k < C + 2; k++) { E[k] = 0; O[k] = 0; }
@@ -295,7 +295,7 @@ MPB_DEVI void acc_sqr(uint32_t (&W)[2 * C + 1], const uint32_t (&x)[C]) {
 // W[0..C) += x*y mod 2^{32C}
 template <int C>
 MPB_DEVI void acc_lo(uint32_t (&W)[2 * C + 1], const uint32_t (&x)[C], const uint32_t (&y)[C]) {
-    uint32_t E[C], O[C];
+    uint32_t E[2 * C], O[2 * C];
     bp_lo<C>(x, y, E, O);
     w_add_trunc<0, C, 0>(W, E);
     w_add_trunc<1, C - 1, 0>(W, O);
@@ -303,7 +303,7 @@ MPB_DEVI void acc_lo(uint32_t (&W)[2 * C + 1], const uint32_t (&x)[C], const uin
 // W[0..C+1] += truncated high part (relative to block position C-1)
 template <int C>
 MPB_DEVI void acc_hi(uint32_t (&W)[2 * C + 1], const uint32_t (&x)[C], const uint32_t (&y)[C]) {
-    uint32_t E[C + 2], O[C + 2];
+    uint32_t E[2 * C], O[2 * C];
     bp_hi<C>(x, y, E, O);
     w_add<0, C + 1, 0>(W, E);
     w_add<0, C + 1, 1>(W, O);

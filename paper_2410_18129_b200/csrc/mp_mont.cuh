@@ -31,30 +31,25 @@
 namespace mpb {
 
 // ----------------------------------------------------------------- accessors
-// Global memory, word-sliced: chunk q of operand k at base[q*stride + k] (uint4 units).
-struct GArr {
+// Word-sliced global array: chunk q (4 limbs, 16 bytes) of this thread's number at p[q*stride].
+struct Arr {
     uint4* p;
     size_t stride;
     MPB_DEVI uint4 ld(int q) const { return p[(size_t)q * stride]; }
     MPB_DEVI void st(int q, uint4 v) const { p[(size_t)q * stride] = v; }
-};
-// Read-only global input (non-coherent path).
-struct GIn {
-    const uint4* p;
-    size_t stride;
-    MPB_DEVI uint4 ld(int q) const { return __ldg(p + (size_t)q * stride); }
+    MPB_DEVI Arr at(int chunk) const { return Arr{p + (size_t)chunk * stride, stride}; }
 };
 
-template <int C, class A>
-MPB_DEVI void ldb(const A& a, int blk, uint32_t (&x)[C]) {
+template <int C>
+MPB_DEVI void ldb(const Arr& a, int blk, uint32_t (&x)[C]) {
 #pragma unroll
     for (int q = 0; q < C / 4; q++) {
         uint4 v = a.ld(blk * (C / 4) + q);
         x[4 * q] = v.x; x[4 * q + 1] = v.y; x[4 * q + 2] = v.z; x[4 * q + 3] = v.w;
     }
 }
-template <int C, int N, class A>
-MPB_DEVI void stb(const A& a, int blk, const uint32_t (&x)[N]) {
+template <int C, int N>
+MPB_DEVI void stb(const Arr& a, int blk, const uint32_t (&x)[N]) {
     static_assert(N >= C, "");
 #pragma unroll
     for (int q = 0; q < C / 4; q++) a.st(blk * (C / 4) + q, make_uint4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]));
@@ -73,85 +68,16 @@ MPB_DEVI void w_shift(uint32_t (&W)[2 * C + 1]) {  // W >>= 32C
     for (int i = C + 1; i <= 2 * C; i++) W[i] = 0;
 }
 
-// --------------------------------------------------------------- phase 1
-// T[0..2L) = X*B (SQR: X^2).  alg:8SBmul / alg:8SBsqu, blocked.
-template <int C, int NB, bool SQR, class AX, class AB, class AT>
-MPB_DEVI void ph_product(const AX& X, const AB& B, const AT& T) {
-    uint32_t W[2 * C + 1];
-    w_zero<C>(W);
-#pragma unroll 1
-    for (int k = 0; k < 2 * NB - 1; k++) {
-        const int s_lo = k - NB + 1 > 0 ? k - NB + 1 : 0;
-        const int s_hi = k < NB - 1 ? k : NB - 1;
-        if (SQR) {
-#pragma unroll 1
-            for (int s = s_lo; 2 * s <= k; s++) {
-                const int t = k - s;
-                uint32_t x[C];
-                ldb<C>(X, s, x);
-                if (s < t) {
-                    uint32_t y[C];
-                    ldb<C>(X, t, y);
-                    acc_mul2<C>(W, x, y);
-                } else {
-                    acc_sqr<C>(W, x);
-                }
-            }
-        } else {
-#pragma unroll 1
-            for (int s = s_lo; s <= s_hi; s++) {
-                uint32_t x[C], y[C];
-                ldb<C>(X, s, x);
-                ldb<C>(B, k - s, y);
-                acc_mul<C>(W, x, y);
-            }
-        }
-        stb<C>(T, k, W);
-        w_shift<C>(W);
-    }
-    stb<C>(T, 2 * NB - 1, W);
-}
-
-// --------------------------------------------------------------- phase 2
-// Q = (T mod R) * N' mod R; also returns orlo = OR of T[0..L-2] and tl1 = T[L-1]
-// (for c_add, eq:c_add P:L459-461, and b, K of the A6/A7 reading).
-template <int C, int NB, class AT, class ANP, class AQ>
-MPB_DEVI void ph_q(const AT& T, const ANP& NP, const AQ& Q, uint32_t& orlo, uint32_t& tl1) {
-    uint32_t W[2 * C + 1];
-    w_zero<C>(W);
-    orlo = 0;
-    tl1 = 0;
-#pragma unroll 1
-    for (int k = 0; k < NB; k++) {
-#pragma unroll 1
-        for (int s = 0; s <= k; s++) {
-            uint32_t x[C], y[C];
-            ldb<C>(T, s, x);
-            ldb<C>(NP, k - s, y);
-            if (s == k) {  // first (and only) time block T_k is loaded with t == 0
-#pragma unroll
-                for (int i = 0; i < C - 1; i++) orlo |= x[i];
-                if (k == NB - 1) tl1 = x[C - 1];
-                else orlo |= x[C - 1];
-            }
-            if (k < NB - 1) acc_mul<C>(W, x, y);
-            else acc_lo<C>(W, x, y);
-        }
-        stb<C>(Q, k, W);
-        w_shift<C>(W);
-    }
-}
-
 // ------------------------------------------------ shared tail: C, D = C - N
 // Block j of H (window words 0..C-1) becomes block j of C = T_hi + H + carry (truncated) or
 // of C itself (full); C is parked in T block NB+j and D = C - N - borrow goes to OUT block j.
-template <int C, int NB, bool ADD_THI, class AT, class AN, class AOUT>
-MPB_DEVI void emit_block(const uint32_t (&W)[2 * C + 1], int j, const AT& T, const AN& N, const AOUT& OUT,
-                         uint32_t& carry, uint32_t& borrow) {
+template <int C, int NB>
+MPB_DEVI void emit_block(const uint32_t (&W)[2 * C + 1], int j, bool add_thi, const Arr& T, const Arr& N,
+                         const Arr& OUT, uint32_t& carry, uint32_t& borrow) {
     uint32_t c[C];
 #pragma unroll
     for (int i = 0; i < C; i++) c[i] = W[i];
-    if (ADD_THI) {
+    if (add_thi) {
         uint32_t t[C];
         ldb<C>(T, NB + j, t);
         cc_restore(carry);
@@ -170,15 +96,15 @@ MPB_DEVI void emit_block(const uint32_t (&W)[2 * C + 1], int j, const AT& T, con
 }
 
 // OUT = (ctop || !borrow) ? D : C, with D in OUT and C in T[NB..2NB) -- a mask, no branch.
-template <int C, int NB, class AT, class AOUT>
-MPB_DEVI void final_select(const AT& T, const AOUT& OUT, uint32_t ctop, uint32_t borrow) {
+template <int C, int NB>
+MPB_DEVI void final_select(const Arr& T, const Arr& OUT, uint32_t ctop, uint32_t borrow) {
     const uint32_t m = 0u - ((ctop | (borrow ^ 1u)) & 1u);  // all ones: take D = C - N
 #pragma unroll 1
     for (int j = 0; j < NB; j++) {
 #pragma unroll
         for (int q = 0; q < C / 4; q++) {
             uint4 d = OUT.ld(j * (C / 4) + q);
-            uint4 c = T.ld((NB + j) * (C / 4) + q);
+            const uint4 c = T.ld((NB + j) * (C / 4) + q);
             d.x = (d.x & m) | (c.x & ~m);
             d.y = (d.y & m) | (c.y & ~m);
             d.z = (d.z & m) | (c.z & ~m);
@@ -188,139 +114,174 @@ MPB_DEVI void final_select(const AT& T, const AOUT& OUT, uint32_t ctop, uint32_t
     }
 }
 
-// ------------------------------------------------------ phase 3, truncated
-// alg:trunc_montred lines 2-4: C = floor(T/R) + qnhat + c_add with
-//   qnhat = floor(S'/2^32) + [S mod 2^32 > K],  S' = sum of partial products of weight >= L-1
-//   (lo of i+j = L-1 and up, hi of i+j = L-2 and up), K = (-T[L-1] - b) mod 2^32,
-//   b = [T mod 2^{32(L-1)} != 0], c_add = [T mod R != 0].
-template <int C, int NB, class AQ, class AN, class AT, class AOUT>
-MPB_DEVI void ph_hi_trunc(const AQ& Q, const AN& N, const AT& T, const AOUT& OUT, uint32_t orlo, uint32_t tl1) {
-    const uint32_t b = orlo != 0u ? 1u : 0u;
-    const uint32_t c_add = (orlo | tl1) != 0u ? 1u : 0u;
-    const uint32_t K = 0u - tl1 - b;
-    uint32_t W[2 * C + 1];
-    w_zero<C>(W);
-    // corners: block column NB-2 contributes hi(q_s[C-1] * N_t[C-1]) at global position L-1
-#pragma unroll 1
-    for (int s = 0; s + 2 <= NB; s++) {
-        const uint4 qv = Q.ld(s * (C / 4) + C / 4 - 1);
-        const uint4 nv = N.ld((NB - 2 - s) * (C / 4) + C / 4 - 1);
-        asm volatile("mad.hi.cc.u32 %0, %2, %3, %0;\n\taddc.u32 %1, %1, 0;" : "+r"(W[0]), "+r"(W[1]) : "r"(qv.w), "r"(nv.w));
-    }
-    // block column NB-1: truncated high parts, relative to global position L-1
-#pragma unroll 1
-    for (int s = 0; s < NB; s++) {
-        uint32_t x[C], y[C];
-        ldb<C>(Q, s, x);
-        ldb<C>(N, NB - 1 - s, y);
-        acc_hi<C>(W, x, y);
-    }
-    // exact carry out of column L-1 (eq:TqN / eq:qnhat under the A6/A7 reading)
-    const uint32_t corr = W[0] > K ? 1u : 0u;
-#pragma unroll
-    for (int i = 0; i < 2 * C; i++) W[i] = W[i + 1];
-    W[2 * C] = 0;
-    add_first(W[0], corr);
-#pragma unroll
-    for (int i = 1; i <= C; i++) add_next(W[i], 0u);
-    absorb(W[C + 1]);
-    // block columns NB .. 2NB-2 (global offset k*C), full block products
-    uint32_t carry = c_add, borrow = 0;
-#pragma unroll 1
-    for (int k = NB; k < 2 * NB - 1; k++) {
-#pragma unroll 1
-        for (int s = k - NB + 1; s < NB; s++) {
-            uint32_t x[C], y[C];
-            ldb<C>(Q, s, x);
-            ldb<C>(N, k - s, y);
-            acc_mul<C>(W, x, y);
-        }
-        emit_block<C, NB, true>(W, k - NB, T, N, OUT, carry, borrow);
-        w_shift<C>(W);
-    }
-    emit_block<C, NB, true>(W, NB - 1, T, N, OUT, carry, borrow);
-    final_select<C, NB>(T, OUT, carry, borrow);
-}
+// ------------------------------------------------------------ the engine
+// One generic block-column engine runs every phase of every Montgomery operation, so each
+// block primitive exists once in a kernel's code (the hot loop stays inside the instruction
+// cache).  Phases:
+//   PH_MUL / PH_SQR  DST = AX*AY (AX^2): alg:8SBmul / alg:8SBsqu, blocked
+//   PH_Q             DST = (AX mod R)*AY mod R, AX = T, AY = N'             (alg:montred l.1)
+//                    also orlo = OR T[0..L-2], tl1 = T[L-1] (eq:c_add; A6)
+//   PH_HI            AX = q, AY = N.  TRUNC: alg:trunc_montred lines 2-4 with
+//                    qnhat from the partial products of weight >= L-1 and the exact carry
+//                    correction [S mod 2^32 > K] (Theorem 2).
+//                    FULL: alg:8MontRed lines 2-3, C = (T + q*N)/R.
+//                    Then D = C - N and a masked select give the canonical result in OUT.
+enum { PH_MUL = 0, PH_SQR = 1, PH_Q = 2, PH_HI = 3 };
+enum { OP_MUL = 0, OP_MUL2 = 1, OP_SQR = 2, OP_LO = 3, OP_HI = 4 };
 
-// ----------------------------------------------------------- phase 3, full
-// alg:8MontRed lines 2-3: C = (T + q*N) / R with the whole q*N product.
-template <int C, int NB, class AQ, class AN, class AT, class AOUT>
-MPB_DEVI void ph_hi_full(const AQ& Q, const AN& N, const AT& T, const AOUT& OUT) {
+template <int C, int NB, bool TRUNC>
+MPB_DEVI void engine(int ph, const Arr& AX, const Arr& AY, const Arr& DST, const Arr& T, const Arr& N,
+                     const Arr& OUT, uint32_t& orlo, uint32_t& tl1) {
     uint32_t W[2 * C + 1];
     w_zero<C>(W);
     uint32_t carry = 0, borrow = 0;
+    int k0 = 0, k1 = 2 * NB - 1;
+    if (ph == PH_Q) k1 = NB;
+    if (ph == PH_HI) {
+        if (TRUNC) {
+            k0 = NB - 1;
+            const uint32_t b = orlo != 0u ? 1u : 0u;
+            carry = (orlo | tl1) != 0u ? 1u : 0u;  // c_add = [T mod R != 0]
+            // corners: block column NB-2 contributes hi(q_s[C-1] * N_t[C-1]) at position L-1
 #pragma unroll 1
-    for (int k = 0; k < 2 * NB; k++) {
-        if (k < 2 * NB - 1) {
-            const int s_lo = k - NB + 1 > 0 ? k - NB + 1 : 0;
-            const int s_hi = k < NB - 1 ? k : NB - 1;
+            for (int s = 0; s + 2 <= NB; s++) {
+                const uint4 qv = AX.ld(s * (C / 4) + C / 4 - 1);
+                const uint4 nv = AY.ld((NB - 2 - s) * (C / 4) + C / 4 - 1);
+                asm volatile("mad.hi.cc.u32 %0, %2, %3, %0;\n\taddc.u32 %1, %1, 0;"
+                             : "+r"(W[0]), "+r"(W[1]) : "r"(qv.w), "r"(nv.w));
+            }
+            orlo = 0u - tl1 - b;  // reuse: K = (-T[L-1] - b) mod 2^32
+        } else {
+            k1 = 2 * NB;
+        }
+    }
 #pragma unroll 1
-            for (int s = s_lo; s <= s_hi; s++) {
-                uint32_t x[C], y[C];
-                ldb<C>(Q, s, x);
-                ldb<C>(N, k - s, y);
-                acc_mul<C>(W, x, y);
+    for (int k = k0; k < k1; k++) {
+        const int s_lo = k - NB + 1 > 0 ? k - NB + 1 : 0;
+        int s_hi = k < NB - 1 ? k : NB - 1;
+        if (ph == PH_SQR) s_hi = k >> 1;
+#pragma unroll 1
+        for (int s = s_lo; s <= s_hi; s++) {
+            const int t = k - s;
+            int op = OP_MUL;
+            if (ph == PH_SQR) op = s < t ? OP_MUL2 : OP_SQR;
+            else if (ph == PH_Q && k == NB - 1) op = OP_LO;
+            else if (ph == PH_HI && TRUNC && k == NB - 1) op = OP_HI;
+            uint32_t x[C], y[C];
+            ldb<C>(AX, s, x);
+            if (op != OP_SQR) ldb<C>(AY, t, y);
+            if (ph == PH_Q && s == k) {  // block T_k is loaded with t == 0 exactly once
+#pragma unroll
+                for (int i = 0; i < C - 1; i++) orlo |= x[i];
+                if (k == NB - 1) tl1 = x[C - 1];
+                else orlo |= x[C - 1];
+            }
+            if (op == OP_SQR) {
+                acc_sqr<C>(W, x);
+            } else if (op == OP_LO) {
+                acc_lo<C>(W, x, y);
+            } else if (op == OP_HI) {
+                acc_hi<C>(W, x, y);
+            } else {
+                uint32_t E[2 * C], O[2 * C];
+                bp_mul<C>(x, y, E, O);
+                w_add<0, 2 * C, 0>(W, E);
+                w_add<1, 2 * C - 1, 0>(W, O);
+                if (op == OP_MUL2) {
+                    w_add<0, 2 * C, 0>(W, E);
+                    w_add<1, 2 * C - 1, 0>(W, O);
+                }
             }
         }
-        {  // + T block k, carry through the whole window
-            uint32_t t[C];
-            ldb<C>(T, k, t);
-            add_first(W[0], t[0]);
+        // ---- end of block column k
+        if (ph != PH_HI) {
+            stb<C>(DST, k, W);
+            w_shift<C>(W);
+        } else if (TRUNC) {
+            if (k == NB - 1) {
+                // exact carry out of column L-1: floor(S/2^32) + [S mod 2^32 > K]
+                const uint32_t corr = W[0] > orlo ? 1u : 0u;
 #pragma unroll
-            for (int i = 1; i < C; i++) add_next(W[i], t[i]);
+                for (int i = 0; i < 2 * C; i++) W[i] = W[i + 1];
+                W[2 * C] = 0;
+                add_first(W[0], corr);
+#pragma unroll
+                for (int i = 1; i <= C; i++) add_next(W[i], 0u);
+                absorb(W[C + 1]);
+            } else {
+                emit_block<C, NB>(W, k - NB, true, T, N, OUT, carry, borrow);
+                w_shift<C>(W);
+            }
+        } else {
+            uint32_t tb[C];  // + T block k, carried through the whole window
+            ldb<C>(T, k, tb);
+            add_first(W[0], tb[0]);
+#pragma unroll
+            for (int i = 1; i < C; i++) add_next(W[i], tb[i]);
 #pragma unroll
             for (int i = C; i < 2 * C; i++) add_next(W[i], 0u);
             absorb(W[2 * C]);
+            if (k >= NB) emit_block<C, NB>(W, k - NB, false, T, N, OUT, carry, borrow);
+            w_shift<C>(W);
         }
-        if (k >= NB) emit_block<C, NB, false>(W, k - NB, T, N, OUT, carry, borrow);
-        w_shift<C>(W);
     }
-    final_select<C, NB>(T, OUT, W[0], borrow);
+    if (ph == PH_MUL || ph == PH_SQR) stb<C>(DST, 2 * NB - 1, W);
+    if (ph == PH_HI) {
+        if (TRUNC) emit_block<C, NB>(W, NB - 1, true, T, N, OUT, carry, borrow);
+        final_select<C, NB>(T, OUT, TRUNC ? carry : W[0], borrow);
+    }
 }
 
-// ------------------------------------------------------------ compositions
-// OUT = X*B*R^-1 mod N (SQR: X^2*R^-1 mod N), canonical.  T: 2L-word scratch, Q: L-word scratch.
-template <int C, int NB, bool TRUNC, bool SQR, class AX, class AB, class AN, class ANP, class AT, class AQ, class AOUT>
-MPB_DEVI void mont_mul(const AX& X, const AB& B, const AN& N, const ANP& NP, const AT& T, const AQ& Q, const AOUT& OUT) {
-    ph_product<C, NB, SQR>(X, B, T);
-    uint32_t orlo, tl1;
-    ph_q<C, NB>(T, NP, Q, orlo, tl1);
-    if (TRUNC) ph_hi_trunc<C, NB>(Q, N, T, OUT, orlo, tl1);
-    else ph_hi_full<C, NB>(Q, N, T, OUT);
-}
+// Montgomery operation through the engine (single call site for all phases).
+//   mode MUL:  OUT = X*B*R^-1 mod N      mode SQR: OUT = X^2*R^-1 mod N
+//   mode REDC: OUT = T*R^-1 mod N for the 2L-word T already in scratch T
+enum { MODE_MUL = 0, MODE_SQR = 1, MODE_REDC = 2 };
 
-// OUT = T*R^-1 mod N for the 2L-word T held in scratch T (T is consumed).
-template <int C, int NB, bool TRUNC, class AN, class ANP, class AT, class AQ, class AOUT>
-MPB_DEVI void mont_redc(const AN& N, const ANP& NP, const AT& T, const AQ& Q, const AOUT& OUT) {
-    uint32_t orlo, tl1;
-    ph_q<C, NB>(T, NP, Q, orlo, tl1);
-    if (TRUNC) ph_hi_trunc<C, NB>(Q, N, T, OUT, orlo, tl1);
-    else ph_hi_full<C, NB>(Q, N, T, OUT);
+template <int C, int NB, bool TRUNC>
+MPB_DEVI void mont_op(int mode, const Arr& X, const Arr& B, const Arr& N, const Arr& NP, const Arr& T, const Arr& Q,
+                      const Arr& OUT) {
+    uint32_t orlo = 0, tl1 = 0;
+#pragma unroll 1
+    for (int step = mode == MODE_REDC ? 1 : 0; step < 3; step++) {
+        const int ph = step == 0 ? (mode == MODE_SQR ? PH_SQR : PH_MUL) : (step == 1 ? PH_Q : PH_HI);
+        const Arr ax = step == 0 ? X : (step == 1 ? T : Q);
+        const Arr ay = step == 0 ? B : (step == 1 ? NP : N);
+        const Arr dst = step == 0 ? T : Q;
+        engine<C, NB, TRUNC>(ph, ax, ay, dst, T, N, OUT, orlo, tl1);
+    }
 }
 
 // ---------------------------------------------------------- CT table select
 // OUT = G[idx] by a masked scan of every entry ("constant-time batch selection").
-// Entry e, chunk q lives at chunk index e*(L/4) + q of accessor G.
-template <int L, class AG, class AOUT>
-MPB_DEVI void ct_select(const AG& G, int nent, uint32_t idx, const AOUT& OUT) {
-    uint4 acc[L / 4];
-#pragma unroll
-    for (int q = 0; q < L / 4; q++) acc[q] = make_uint4(0, 0, 0, 0);
+// Entry e, chunk q lives at chunk index e*(L/4) + q of G.  Chunks go in groups of 8 so the
+// accumulators stay in registers at every L.
+template <int L>
+MPB_DEVI void ct_select(const Arr& G, int nent, uint32_t idx, const Arr& OUT) {
+    constexpr int Q4 = L / 4, GRP = 8;
 #pragma unroll 1
-    for (int e = 0; e < nent; e++) {
-        const uint32_t x = (uint32_t)e ^ idx;
-        const uint32_t m = 0u - ((x - 1u) >> 31);  // all ones iff e == idx (x < 2^31)
+    for (int g0 = 0; g0 < Q4; g0 += GRP) {
+        uint4 acc[GRP];
 #pragma unroll
-        for (int q = 0; q < L / 4; q++) {
-            const uint4 v = G.ld(e * (L / 4) + q);
-            acc[q].x |= v.x & m;
-            acc[q].y |= v.y & m;
-            acc[q].z |= v.z & m;
-            acc[q].w |= v.w & m;
+        for (int q = 0; q < GRP; q++) acc[q] = make_uint4(0, 0, 0, 0);
+#pragma unroll 1
+        for (int e = 0; e < nent; e++) {
+            const uint32_t x = (uint32_t)e ^ idx;
+            const uint32_t m = 0u - ((x - 1u) >> 31);  // all ones iff e == idx (x < 2^31)
+#pragma unroll
+            for (int q = 0; q < GRP; q++) {
+                if (g0 + q < Q4) {
+                    const uint4 v = G.ld(e * Q4 + g0 + q);
+                    acc[q].x |= v.x & m;
+                    acc[q].y |= v.y & m;
+                    acc[q].z |= v.z & m;
+                    acc[q].w |= v.w & m;
+                }
+            }
         }
-    }
 #pragma unroll
-    for (int q = 0; q < L / 4; q++) OUT.st(q, acc[q]);
+        for (int q = 0; q < GRP; q++)
+            if (g0 + q < Q4) OUT.st(g0 + q, acc[q]);
+    }
 }
 
 }  // namespace mpb
