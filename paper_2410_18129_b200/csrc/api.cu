@@ -328,6 +328,14 @@ int mpb_modexp_host(const uint32_t* N, const uint32_t* base, const uint32_t* exp
     const size_t ws_bytes = mont_batch_modexp_ct_workspace(count, bits, window, 0);
     const size_t setup_bytes = mont_batch_setup_workspace(count, bits);
     uint8_t* dev = nullptr;
+    {  // keep the stream-ordered pool's memory between calls (no re-mapping every call)
+        int devid = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&devid) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, devid) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
     // 7 arrays of L limbs (N, N', R2, base, exp, out, staging) + workspace
     const size_t total = 7 * nb + (ws_bytes > setup_bytes ? ws_bytes : setup_bytes) + 256;
     if (cudaMallocAsync((void**)&dev, total, s) != cudaSuccess) return fail(MPB_ECUDA, "cudaMallocAsync failed");

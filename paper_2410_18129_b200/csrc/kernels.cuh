@@ -12,12 +12,23 @@
 namespace mpb {
 
 constexpr int kThreads = 128;
+#ifndef MPB_MODEXP_MINB
+#define MPB_MODEXP_MINB 1
+#endif
 
 MPB_DEVI size_t tid_global() { return (size_t)blockIdx.x * blockDim.x + threadIdx.x; }
 // word-sliced accessor for operand k of an array with `count` operands
 MPB_DEVI Arr arr(const uint32_t* base, size_t count, size_t k) {
-    return Arr{reinterpret_cast<uint4*>(const_cast<uint32_t*>(base)) + k, count};
+    return Arr{reinterpret_cast<char*>(const_cast<uint32_t*>(base)) + k * 16, (uint32_t)(count * 16)};
 }
+// this thread's staging area in dynamic shared memory (2 buffers x 2 blocks x C/4 chunks)
+template <int C>
+MPB_DEVI Stage stage() {
+    extern __shared__ uint4 smem_stage[];
+    return Stage{(uint32_t)__cvta_generic_to_shared(smem_stage + threadIdx.x), (uint32_t)(blockDim.x * 16)};
+}
+template <int C>
+constexpr size_t stage_bytes() { return (size_t)kThreads * 4 * (C / 4) * 16; }
 // word i of operand k (32-bit access)
 MPB_DEVI uint32_t word_at(const uint32_t* base, size_t count, size_t k, int i) {
     return __ldg(base + ((size_t)(i >> 2) * count + k) * 4 + (i & 3));
@@ -32,7 +43,7 @@ __global__ void __launch_bounds__(kThreads) k_mp_mul(const uint32_t* __restrict_
     uint32_t orlo = 0, tl1 = 0;
     const Arr C_ = arr(c, count, k);
     engine<C, NB, true>(SQR ? PH_SQR : PH_MUL, arr(a, count, k), arr(SQR ? a : b, count, k), C_, C_, C_, C_, orlo,
-                        tl1);
+                        tl1, stage<C>());
 }
 
 // workspace for the mont kernels: T (2L) then Q (L), word-sliced with stride count
@@ -45,7 +56,7 @@ __global__ void __launch_bounds__(kThreads) k_mont_mul(const uint32_t* __restric
     if (k >= count) return;
     const Arr T = arr(ws, count, k), Q = arr(ws + (size_t)2 * L * count, count, k);
     mont_op<C, NB, TRUNC>(SQR ? MODE_SQR : MODE_MUL, arr(a, count, k), arr(SQR ? a : b, count, k), arr(N, count, k),
-                          arr(NP, count, k), T, Q, arr(c, count, k));
+                          arr(NP, count, k), T, Q, arr(c, count, k), stage<C>());
 }
 
 template <int C, int NB, bool TRUNC>
@@ -59,7 +70,7 @@ __global__ void __launch_bounds__(kThreads) k_mont_redc(const uint32_t* __restri
     const Arr Ti = arr(Tin, count, k);
 #pragma unroll 1
     for (int q = 0; q < 2 * L / 4; q++) T.st(q, Ti.ld(q));
-    mont_op<C, NB, TRUNC>(MODE_REDC, T, T, arr(N, count, k), arr(NP, count, k), T, Q, arr(c, count, k));
+    mont_op<C, NB, TRUNC>(MODE_REDC, T, T, arr(N, count, k), arr(NP, count, k), T, Q, arr(c, count, k), stage<C>());
 }
 
 // ------------------------------------------------------------------- modexp
@@ -74,7 +85,7 @@ __global__ void __launch_bounds__(kThreads) k_mont_redc(const uint32_t* __restri
 //   last op          out = REDC(Y)
 // workspace per operand (word-sliced, stride count): G (2^w * L) | Y (L) | T (2L) | Q (L) | S (L)
 template <int C, int NB, bool TRUNC>
-__global__ void __launch_bounds__(kThreads) k_modexp(const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP,
+__global__ void __launch_bounds__(kThreads, MPB_MODEXP_MINB) k_modexp(const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP,
                                                      const uint32_t* __restrict__ R2, const uint32_t* __restrict__ base,
                                                      const uint32_t* __restrict__ exp, uint32_t* __restrict__ out,
                                                      size_t count, int bits, int w, uint32_t* ws) {
@@ -94,6 +105,7 @@ __global__ void __launch_bounds__(kThreads) k_modexp(const uint32_t* __restrict_
     const Arr S = arr(p, count, k);
     const Arr Nn = arr(N, count, k), NPn = arr(NP, count, k), R2n = arr(R2, count, k), Bn = arr(base, count, k);
     const Arr On = arr(out, count, k);
+    const Stage sg = stage<C>();
 
     const int nwin = (bits + w - 1) / w;
     const int per_win = w + 2;
@@ -140,7 +152,7 @@ __global__ void __launch_bounds__(kThreads) k_modexp(const uint32_t* __restrict_
                 T.st(Q4 + q, make_uint4(0, 0, 0, 0));
             }
         }
-        mont_op<C, NB, TRUNC>(mode, X, B, Nn, NPn, T, Q, O);
+        mont_op<C, NB, TRUNC>(mode, X, B, Nn, NPn, T, Q, O, sg);
     }
 }
 
@@ -148,33 +160,33 @@ inline unsigned grid_for(size_t n) { return (unsigned)((n + kThreads - 1) / kThr
 
 template <int C, int NB>
 void Launch<C, NB>::mp_mul(const uint32_t* a, const uint32_t* b, uint32_t* c, size_t count, bool sqr, cudaStream_t s) {
-    if (sqr) k_mp_mul<C, NB, true><<<grid_for(count), kThreads, 0, s>>>(a, a, c, count);
-    else k_mp_mul<C, NB, false><<<grid_for(count), kThreads, 0, s>>>(a, b, c, count);
+    if (sqr) k_mp_mul<C, NB, true><<<grid_for(count), kThreads, stage_bytes<C>(), s>>>(a, a, c, count);
+    else k_mp_mul<C, NB, false><<<grid_for(count), kThreads, stage_bytes<C>(), s>>>(a, b, c, count);
 }
 template <int C, int NB>
 void Launch<C, NB>::mont_mul(const uint32_t* a, const uint32_t* b, const uint32_t* N, const uint32_t* NP, uint32_t* c,
                              size_t count, bool trunc, bool sqr, uint32_t* ws, cudaStream_t s) {
     const unsigned g = grid_for(count);
     if (trunc) {
-        if (sqr) k_mont_mul<C, NB, true, true><<<g, kThreads, 0, s>>>(a, a, N, NP, c, count, ws);
-        else k_mont_mul<C, NB, true, false><<<g, kThreads, 0, s>>>(a, b, N, NP, c, count, ws);
+        if (sqr) k_mont_mul<C, NB, true, true><<<g, kThreads, stage_bytes<C>(), s>>>(a, a, N, NP, c, count, ws);
+        else k_mont_mul<C, NB, true, false><<<g, kThreads, stage_bytes<C>(), s>>>(a, b, N, NP, c, count, ws);
     } else {
-        if (sqr) k_mont_mul<C, NB, false, true><<<g, kThreads, 0, s>>>(a, a, N, NP, c, count, ws);
-        else k_mont_mul<C, NB, false, false><<<g, kThreads, 0, s>>>(a, b, N, NP, c, count, ws);
+        if (sqr) k_mont_mul<C, NB, false, true><<<g, kThreads, stage_bytes<C>(), s>>>(a, a, N, NP, c, count, ws);
+        else k_mont_mul<C, NB, false, false><<<g, kThreads, stage_bytes<C>(), s>>>(a, b, N, NP, c, count, ws);
     }
 }
 template <int C, int NB>
 void Launch<C, NB>::mont_redc(const uint32_t* T, const uint32_t* N, const uint32_t* NP, uint32_t* c, size_t count,
                               bool trunc, uint32_t* ws, cudaStream_t s) {
-    if (trunc) k_mont_redc<C, NB, true><<<grid_for(count), kThreads, 0, s>>>(T, N, NP, c, count, ws);
-    else k_mont_redc<C, NB, false><<<grid_for(count), kThreads, 0, s>>>(T, N, NP, c, count, ws);
+    if (trunc) k_mont_redc<C, NB, true><<<grid_for(count), kThreads, stage_bytes<C>(), s>>>(T, N, NP, c, count, ws);
+    else k_mont_redc<C, NB, false><<<grid_for(count), kThreads, stage_bytes<C>(), s>>>(T, N, NP, c, count, ws);
 }
 template <int C, int NB>
 void Launch<C, NB>::modexp(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
                            const uint32_t* exp, uint32_t* out, size_t count, int bits, int window, bool trunc,
                            uint32_t* ws, cudaStream_t s) {
-    if (trunc) k_modexp<C, NB, true><<<grid_for(count), kThreads, 0, s>>>(N, NP, R2, base, exp, out, count, bits, window, ws);
-    else k_modexp<C, NB, false><<<grid_for(count), kThreads, 0, s>>>(N, NP, R2, base, exp, out, count, bits, window, ws);
+    if (trunc) k_modexp<C, NB, true><<<grid_for(count), kThreads, stage_bytes<C>(), s>>>(N, NP, R2, base, exp, out, count, bits, window, ws);
+    else k_modexp<C, NB, false><<<grid_for(count), kThreads, stage_bytes<C>(), s>>>(N, NP, R2, base, exp, out, count, bits, window, ws);
 }
 
 }  // namespace mpb

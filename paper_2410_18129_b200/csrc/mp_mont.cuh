@@ -31,14 +31,39 @@
 namespace mpb {
 
 // ----------------------------------------------------------------- accessors
-// Word-sliced global array: chunk q (4 limbs, 16 bytes) of this thread's number at p[q*stride].
+// Word-sliced global array: chunk q (4 limbs, 16 bytes) of this thread's number at p + q*sb
+// (sb = count * 16 bytes).  The chunk address is one IMAD.WIDE.U32 (32-bit q times 32-bit sb
+// plus the 64-bit base).
 struct Arr {
-    uint4* p;
-    size_t stride;
-    MPB_DEVI uint4 ld(int q) const { return p[(size_t)q * stride]; }
-    MPB_DEVI void st(int q, uint4 v) const { p[(size_t)q * stride] = v; }
-    MPB_DEVI Arr at(int chunk) const { return Arr{p + (size_t)chunk * stride, stride}; }
+    char* p;
+    uint32_t sb;
+    MPB_DEVI uint4* addr(int q) const { return reinterpret_cast<uint4*>(p + (size_t)(uint32_t)q * sb); }
+    MPB_DEVI uint4 ld(int q) const { return *addr(q); }
+    MPB_DEVI uint4 ld_stream(int q) const { return __ldcs(addr(q)); }  // evict-first (table scans)
+    MPB_DEVI void st(int q, uint4 v) const { *addr(q) = v; }
+    MPB_DEVI Arr at(int chunk) const { return Arr{p + (size_t)(uint32_t)chunk * sb, sb}; }
 };
+
+// Per-thread shared-memory staging for the operand blocks of the next block product
+// (double buffered, filled by cp.async while the current block product runs).
+// Chunk c of this thread lives at base + c*cs bytes (cs = blockDim * 16: conflict-free LDS.128).
+struct Stage {
+    uint32_t base;
+    uint32_t cs;
+};
+MPB_DEVI void cp_async16(uint32_t saddr, const void* g) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
+}
+MPB_DEVI void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+MPB_DEVI void cp_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+MPB_DEVI uint4 lds128(uint32_t saddr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(saddr));
+    return v;
+}
 
 template <int C>
 MPB_DEVI void ldb(const Arr& a, int blk, uint32_t (&x)[C]) {
@@ -131,7 +156,7 @@ enum { OP_MUL = 0, OP_MUL2 = 1, OP_SQR = 2, OP_LO = 3, OP_HI = 4 };
 
 template <int C, int NB, bool TRUNC>
 MPB_DEVI void engine(int ph, const Arr& AX, const Arr& AY, const Arr& DST, const Arr& T, const Arr& N,
-                     const Arr& OUT, uint32_t& orlo, uint32_t& tl1) {
+                     const Arr& OUT, uint32_t& orlo, uint32_t& tl1, const Stage& sg) {
     uint32_t W[2 * C + 1];
     w_zero<C>(W);
     uint32_t carry = 0, borrow = 0;
@@ -155,11 +180,46 @@ MPB_DEVI void engine(int ph, const Arr& AX, const Arr& AY, const Arr& DST, const
             k1 = 2 * NB;
         }
     }
+    // pair (k, s) ranges of block column k; pairs are prefetched one ahead into shared memory
+    auto s_lo_of = [&](int k) { return k - NB + 1 > 0 ? k - NB + 1 : 0; };
+    auto s_hi_of = [&](int k) {
+        int h = k < NB - 1 ? k : NB - 1;
+        if (ph == PH_SQR) h = k >> 1;
+        return h;
+    };
+    auto advance = [&](int& k, int& s) -> bool {  // next pair after (k, s), false if none
+        if (s < s_hi_of(k)) {
+            s++;
+            return true;
+        }
+#pragma unroll 1
+        for (k = k + 1; k < k1; k++) {
+            s = s_lo_of(k);
+            if (s <= s_hi_of(k)) return true;
+        }
+        return false;
+    };
+    auto issue = [&](int k, int s, int buf) {
+        const uint32_t b = sg.base + (uint32_t)(buf * 2 * (C / 4)) * sg.cs;
+#pragma unroll
+        for (int q = 0; q < C / 4; q++) cp_async16(b + q * sg.cs, AX.addr(s * (C / 4) + q));
+        if (!(ph == PH_SQR && 2 * s == k)) {
+#pragma unroll
+            for (int q = 0; q < C / 4; q++) cp_async16(b + (C / 4 + q) * sg.cs, AY.addr((k - s) * (C / 4) + q));
+        }
+        cp_commit();
+    };
+    {
+        int fk = k0, fs = s_lo_of(k0) - 1;
+        if (k0 < k1 && s_lo_of(k0) <= s_hi_of(k0)) fs = s_lo_of(k0);
+        else if (!advance(fk, fs)) fk = -1;
+        if (fk >= 0) issue(fk, fs, 0);
+    }
+    int buf = 0;
 #pragma unroll 1
     for (int k = k0; k < k1; k++) {
-        const int s_lo = k - NB + 1 > 0 ? k - NB + 1 : 0;
-        int s_hi = k < NB - 1 ? k : NB - 1;
-        if (ph == PH_SQR) s_hi = k >> 1;
+        const int s_lo = s_lo_of(k);
+        const int s_hi = s_hi_of(k);
 #pragma unroll 1
         for (int s = s_lo; s <= s_hi; s++) {
             const int t = k - s;
@@ -167,9 +227,32 @@ MPB_DEVI void engine(int ph, const Arr& AX, const Arr& AY, const Arr& DST, const
             if (ph == PH_SQR) op = s < t ? OP_MUL2 : OP_SQR;
             else if (ph == PH_Q && k == NB - 1) op = OP_LO;
             else if (ph == PH_HI && TRUNC && k == NB - 1) op = OP_HI;
+            {
+                int nk = k, ns = s;
+                if (advance(nk, ns)) {
+                    issue(nk, ns, buf ^ 1);
+                    cp_wait<1>();
+                } else {
+                    cp_wait<0>();
+                }
+            }
             uint32_t x[C], y[C];
-            ldb<C>(AX, s, x);
-            if (op != OP_SQR) ldb<C>(AY, t, y);
+            {
+                const uint32_t b = sg.base + (uint32_t)(buf * 2 * (C / 4)) * sg.cs;
+#pragma unroll
+                for (int q = 0; q < C / 4; q++) {
+                    const uint4 v = lds128(b + q * sg.cs);
+                    x[4 * q] = v.x; x[4 * q + 1] = v.y; x[4 * q + 2] = v.z; x[4 * q + 3] = v.w;
+                }
+                if (op != OP_SQR) {
+#pragma unroll
+                    for (int q = 0; q < C / 4; q++) {
+                        const uint4 v = lds128(b + (C / 4 + q) * sg.cs);
+                        y[4 * q] = v.x; y[4 * q + 1] = v.y; y[4 * q + 2] = v.z; y[4 * q + 3] = v.w;
+                    }
+                }
+            }
+            buf ^= 1;
             if (ph == PH_Q && s == k) {  // block T_k is loaded with t == 0 exactly once
 #pragma unroll
                 for (int i = 0; i < C - 1; i++) orlo |= x[i];
@@ -239,7 +322,7 @@ enum { MODE_MUL = 0, MODE_SQR = 1, MODE_REDC = 2 };
 
 template <int C, int NB, bool TRUNC>
 MPB_DEVI void mont_op(int mode, const Arr& X, const Arr& B, const Arr& N, const Arr& NP, const Arr& T, const Arr& Q,
-                      const Arr& OUT) {
+                      const Arr& OUT, const Stage& sg) {
     uint32_t orlo = 0, tl1 = 0;
 #pragma unroll 1
     for (int step = mode == MODE_REDC ? 1 : 0; step < 3; step++) {
@@ -247,7 +330,7 @@ MPB_DEVI void mont_op(int mode, const Arr& X, const Arr& B, const Arr& N, const 
         const Arr ax = step == 0 ? X : (step == 1 ? T : Q);
         const Arr ay = step == 0 ? B : (step == 1 ? NP : N);
         const Arr dst = step == 0 ? T : Q;
-        engine<C, NB, TRUNC>(ph, ax, ay, dst, T, N, OUT, orlo, tl1);
+        engine<C, NB, TRUNC>(ph, ax, ay, dst, T, N, OUT, orlo, tl1, sg);
     }
 }
 
@@ -270,7 +353,7 @@ MPB_DEVI void ct_select(const Arr& G, int nent, uint32_t idx, const Arr& OUT) {
 #pragma unroll
             for (int q = 0; q < GRP; q++) {
                 if (g0 + q < Q4) {
-                    const uint4 v = G.ld(e * Q4 + g0 + q);
+                    const uint4 v = G.ld_stream(e * Q4 + g0 + q);
                     acc[q].x |= v.x & m;
                     acc[q].y |= v.y & m;
                     acc[q].z |= v.z & m;
