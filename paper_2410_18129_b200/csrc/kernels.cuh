@@ -13,7 +13,7 @@ namespace mpb {
 
 constexpr int kThreads = 128;
 #ifndef MPB_MODEXP_MINB
-#define MPB_MODEXP_MINB 1
+#define MPB_MODEXP_MINB 3
 #endif
 
 MPB_DEVI size_t tid_global() { return (size_t)blockIdx.x * blockDim.x + threadIdx.x; }
