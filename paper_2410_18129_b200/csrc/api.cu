@@ -8,6 +8,7 @@
 
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -117,13 +118,24 @@ __global__ void k_setup(const uint32_t* __restrict__ N, uint32_t* __restrict__ N
 }
 
 // ------------------------------------------------------------- dispatch
+// Block size for L = 64 (tuning switch, environment MPB_C64 in {8, 16}; default 16).
+int block64() {
+    static int c = [] {
+        const char* e = getenv("MPB_C64");
+        return (e && atoi(e) == 8) ? 8 : 16;
+    }();
+    return c;
+}
+
 // Compiled shapes: (C, NB) with L = C*NB.
 template <typename F>
 int dispatch_L(int L, F&& f) {
     switch (L) {
         case 16: return f(std::integral_constant<int, 16>{}, std::integral_constant<int, 1>{});
         case 32: return f(std::integral_constant<int, 16>{}, std::integral_constant<int, 2>{});
-        case 64: return f(std::integral_constant<int, 16>{}, std::integral_constant<int, 4>{});
+        case 64:
+            if (block64() == 8) return f(std::integral_constant<int, 8>{}, std::integral_constant<int, 8>{});
+            return f(std::integral_constant<int, 16>{}, std::integral_constant<int, 4>{});
         case 96: return f(std::integral_constant<int, 16>{}, std::integral_constant<int, 6>{});
         case 128: return f(std::integral_constant<int, 16>{}, std::integral_constant<int, 8>{});
         case 132: return f(std::integral_constant<int, 12>{}, std::integral_constant<int, 11>{});

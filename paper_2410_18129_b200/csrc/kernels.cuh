@@ -12,9 +12,18 @@
 namespace mpb {
 
 constexpr int kThreads = 128;
-#ifndef MPB_MODEXP_MINB
-#define MPB_MODEXP_MINB 3
+// resident CTAs per SM the modexp kernel is compiled for (register budget 65536 / (128 * minb))
+template <int C>
+__host__ __device__ constexpr int modexp_min_blocks() { return C >= 12 ? 3 : 5; }
+// entries of the CT table scan kept in flight per step (register budget)
+template <int C>
+__host__ __device__ constexpr int select_unroll() {
+#ifdef MPB_SEL_U
+    return MPB_SEL_U;
+#else
+    return 4;  // measured best at L = 64 (U = 4 entries x 4 chunks in flight; 8 x 4 and 1 x 8 are slower)
 #endif
+}
 
 MPB_DEVI size_t tid_global() { return (size_t)blockIdx.x * blockDim.x + threadIdx.x; }
 // word-sliced accessor for operand k of an array with `count` operands
@@ -85,7 +94,7 @@ __global__ void __launch_bounds__(kThreads) k_mont_redc(const uint32_t* __restri
 //   last op          out = REDC(Y)
 // workspace per operand (word-sliced, stride count): G (2^w * L) | Y (L) | T (2L) | Q (L) | S (L)
 template <int C, int NB, bool TRUNC>
-__global__ void __launch_bounds__(kThreads, MPB_MODEXP_MINB) k_modexp(const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP,
+__global__ void __launch_bounds__(kThreads, modexp_min_blocks<C>()) k_modexp(const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP,
                                                      const uint32_t* __restrict__ R2, const uint32_t* __restrict__ base,
                                                      const uint32_t* __restrict__ exp, uint32_t* __restrict__ out,
                                                      size_t count, int bits, int w, uint32_t* ws) {
@@ -142,7 +151,7 @@ __global__ void __launch_bounds__(kThreads, MPB_MODEXP_MINB) k_modexp(const uint
             const int pos = win * w, wi = pos >> 5, off = pos & 31;
             uint32_t v = word_at(exp, count, k, wi) >> off;
             if (off + w > 32 && wi + 1 < L) v |= word_at(exp, count, k, wi + 1) << (32 - off);
-            ct_select<L>(G, nent, v & ((1u << w) - 1u), O);
+            ct_select<L, select_unroll<C>()>(G, nent, v & ((1u << w) - 1u), O);
             continue;
         }
         if (mode == MODE_REDC) {  // T = X zero-extended to 2L limbs

@@ -20,7 +20,7 @@ struct Launch {
                        cudaStream_t s);
 };
 
-#define MPB_SHAPES(X) X(16, 1) X(16, 2) X(16, 4) X(16, 6) X(16, 8) X(12, 11)
+#define MPB_SHAPES(X) X(16, 1) X(16, 2) X(16, 4) X(16, 6) X(16, 8) X(12, 11) X(8, 8)
 #define MPB_EXTERN(C, NB) extern template struct Launch<C, NB>;
 MPB_SHAPES(MPB_EXTERN)
 #undef MPB_EXTERN

@@ -336,34 +336,45 @@ MPB_DEVI void mont_op(int mode, const Arr& X, const Arr& B, const Arr& N, const 
 
 // ---------------------------------------------------------- CT table select
 // OUT = G[idx] by a masked scan of every entry ("constant-time batch selection").
-// Entry e, chunk q lives at chunk index e*(L/4) + q of G.  Chunks go in groups of 8 so the
-// accumulators stay in registers at every L.
-template <int L>
+// Entry e, chunk q lives at chunk index e*(L/4) + q of G.  The scan is bound by DRAM latency
+// (the tables of all resident operands exceed L2), so it keeps SEL_U entries x SEL_G chunks of
+// loads in flight per step; accumulators stay in registers at every L.
+template <int L, int U>
 MPB_DEVI void ct_select(const Arr& G, int nent, uint32_t idx, const Arr& OUT) {
-    constexpr int Q4 = L / 4, GRP = 8;
+    constexpr int Q4 = L / 4;
+#ifdef MPB_SEL_G
+    constexpr int GRP = MPB_SEL_G;
+#else
+    constexpr int GRP = Q4 % 4 == 0 ? 4 : (Q4 % 3 == 0 ? 3 : (Q4 % 2 == 0 ? 2 : 1));
+#endif
 #pragma unroll 1
     for (int g0 = 0; g0 < Q4; g0 += GRP) {
         uint4 acc[GRP];
 #pragma unroll
         for (int q = 0; q < GRP; q++) acc[q] = make_uint4(0, 0, 0, 0);
 #pragma unroll 1
-        for (int e = 0; e < nent; e++) {
-            const uint32_t x = (uint32_t)e ^ idx;
-            const uint32_t m = 0u - ((x - 1u) >> 31);  // all ones iff e == idx (x < 2^31)
+        for (int e0 = 0; e0 < nent; e0 += U) {
+            uint4 v[U][GRP];
 #pragma unroll
-            for (int q = 0; q < GRP; q++) {
-                if (g0 + q < Q4) {
-                    const uint4 v = G.ld_stream(e * Q4 + g0 + q);
-                    acc[q].x |= v.x & m;
-                    acc[q].y |= v.y & m;
-                    acc[q].z |= v.z & m;
-                    acc[q].w |= v.w & m;
+            for (int u = 0; u < U; u++)
+#pragma unroll
+                for (int q = 0; q < GRP; q++)
+                    v[u][q] = (e0 + u < nent) ? G.ld_stream((e0 + u) * Q4 + g0 + q) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const uint32_t x = (uint32_t)(e0 + u) ^ idx;
+                const uint32_t m = 0u - ((x - 1u) >> 31);  // all ones iff e == idx (x < 2^31)
+#pragma unroll
+                for (int q = 0; q < GRP; q++) {
+                    acc[q].x |= v[u][q].x & m;
+                    acc[q].y |= v[u][q].y & m;
+                    acc[q].z |= v[u][q].z & m;
+                    acc[q].w |= v[u][q].w & m;
                 }
             }
         }
 #pragma unroll
-        for (int q = 0; q < GRP; q++)
-            if (g0 + q < Q4) OUT.st(g0 + q, acc[q]);
+        for (int q = 0; q < GRP; q++) OUT.st(g0 + q, acc[q]);
     }
 }
 

@@ -18,7 +18,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmpb.so")
+LIB_PATH = os.environ.get("MPB_LIB") or os.path.join(_HERE, "libmpb.so")  # MPB_LIB: tuning builds only
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
