@@ -4,9 +4,9 @@
  *
  * Numbers.  Unsigned integers in 32-bit limbs, little-endian (a GMP-style
  * 64-bit little-endian word array is byte-identical).  L = mpb_limbs(bits) = 4*ceil(bits/128)
- * limbs per operand, R = 2^(32L).  Supported L: 16, 32, 64, 96, 128, 132 (bits 481..512,
- * 993..1024, 1985..2048, 2945..3072, 3969..4096, 4097..4224); anything else is
- * MPB_EUNSUPPORTED.
+ * limbs per operand, R = 2^(32L).  Any bits in 1..16384 is supported (L <= 512); larger is
+ * MPB_EUNSUPPORTED.  Kernels work on blocks of C = 16, 12, 8 or 4 limbs (the largest that
+ * divides L); 1024/2048/3072/4096 bits use C = 16, 4108/4154 bits (L = 132) use C = 12.
  *
  * Layout ("word-sliced", the B200 form of the paper's Table 1 word slicing):
  * every device array argument below holds `count` operands of `nlimbs` limbs as
@@ -28,8 +28,8 @@
  * for both REDC modes; `redc` and `algo` never change a result, only speed.
  *
  * Errors.  MPB_EINVAL: null / misaligned / aliasing pointer, redc or algo out of range,
- * window not in 1..6 (SPEC "shape"/"usage" errors).  MPB_EUNSUPPORTED: bits not compiled
- * (SPEC "configuration error").  MPB_ECUDA: launch failure; text via mpb_last_error().
+ * window not in 1..6, workspace too small (SPEC "shape"/"usage" errors).  MPB_EUNSUPPORTED:
+ * bits out of range (SPEC "configuration error").  MPB_ECUDA: launch failure; text via mpb_last_error().
  */
 #ifndef PAPER_2410_18129_MPB_H
 #define PAPER_2410_18129_MPB_H
@@ -42,21 +42,27 @@ extern "C" {
 
 typedef enum { MPB_OK = 0, MPB_EINVAL = -1, MPB_EUNSUPPORTED = -2, MPB_ECUDA = -3 } mpb_status;
 enum { MPB_REDC_FULL = 0, MPB_REDC_TRUNCATED = 1 };
-enum { MPB_ALGO_AUTO = 0, MPB_ALGO_SCHOOLBOOK = 1, MPB_ALGO_KARATSUBA = 2 };
+/* AUTO = the measured crossover; KARATSUBA = one level, KARATSUBA2 = two levels. */
+enum { MPB_ALGO_AUTO = 0, MPB_ALGO_SCHOOLBOOK = 1, MPB_ALGO_KARATSUBA = 2, MPB_ALGO_KARATSUBA2 = 3 };
 
 /* L(bits) = 4*ceil(bits/128); 0 if bits <= 0. */
 int mpb_limbs(int bits);
-/* 1 if bits maps to a compiled limb count. */
+/* 1 if bits is supported (1..16384). */
 int mpb_supported(int bits);
 
 /* Layout: operand-major (count x limbs) <-> word-sliced.  limbs % 4 == 0. */
 int mpb_layout_expand(const uint32_t* src_opmajor, uint32_t* dst, size_t count, int limbs, void* stream);
 int mpb_layout_contract(const uint32_t* src, uint32_t* dst_opmajor, size_t count, int limbs, void* stream);
 
-/* c = a*b, c has 2L limbs (word-sliced with 2L limbs).  alg:8SBmul. */
-int mp_batch_mul(const uint32_t* a, const uint32_t* b, uint32_t* c, size_t count, int bits, int algo, void* stream);
-/* c = a^2, c has 2L limbs.  alg:8SBsqu. */
-int mp_batch_sqr(const uint32_t* a, uint32_t* c, size_t count, int bits, int algo, void* stream);
+/* c = a*b, c has 2L limbs (word-sliced with 2L limbs).  Schoolbook (alg:8SBmul)
+ * or block-aligned subtractive Karatsuba with 1 or 2 levels.  workspace:
+ * mp_batch_workspace(count, bits, algo) bytes (0 for schoolbook: ws may then be NULL). */
+int mp_batch_mul(const uint32_t* a, const uint32_t* b, uint32_t* c, size_t count, int bits, int algo,
+                 void* workspace, size_t workspace_bytes, void* stream);
+/* c = a^2, c has 2L limbs.  alg:8SBsqu, or Karatsuba squaring. */
+int mp_batch_sqr(const uint32_t* a, uint32_t* c, size_t count, int bits, int algo, void* workspace,
+                 size_t workspace_bytes, void* stream);
+size_t mp_batch_workspace(size_t count, int bits, int algo);
 
 /* c = a*b*R^-1 mod N (canonical).  redc = MPB_REDC_TRUNCATED (alg:trunc_montred)
  * or MPB_REDC_FULL (alg:8MontRed).  Nprime is the full (-N)^-1 mod R (limb 0 is

@@ -118,28 +118,24 @@ __global__ void k_setup(const uint32_t* __restrict__ N, uint32_t* __restrict__ N
 }
 
 // ------------------------------------------------------------- dispatch
-// Block size for L = 64 (tuning switch, environment MPB_C64 in {8, 16}; default 16).
-int block64() {
-    static int c = [] {
-        const char* e = getenv("MPB_C64");
-        return (e && atoi(e) == 8) ? 8 : 16;
+// Kernels are instantiated per block size C in {16, 12, 8, 4}; nb = L / C is a runtime
+// argument.  Block size for a limb count: the largest C dividing L (mpb::block_for), unless
+// the environment variable MPB_BLOCK forces one (tuning only).
+int block_of(int L) {
+    static int forced = [] {
+        const char* e = getenv("MPB_BLOCK");
+        return e ? atoi(e) : 0;
     }();
-    return c;
+    if ((forced == 16 || forced == 12 || forced == 8 || forced == 4) && L % forced == 0) return forced;
+    return mpb::block_for(L);
 }
-
-// Compiled shapes: (C, NB) with L = C*NB.
 template <typename F>
 int dispatch_L(int L, F&& f) {
-    switch (L) {
-        case 16: return f(std::integral_constant<int, 16>{}, std::integral_constant<int, 1>{});
-        case 32: return f(std::integral_constant<int, 16>{}, std::integral_constant<int, 2>{});
-        case 64:
-            if (block64() == 8) return f(std::integral_constant<int, 8>{}, std::integral_constant<int, 8>{});
-            return f(std::integral_constant<int, 16>{}, std::integral_constant<int, 4>{});
-        case 96: return f(std::integral_constant<int, 16>{}, std::integral_constant<int, 6>{});
-        case 128: return f(std::integral_constant<int, 16>{}, std::integral_constant<int, 8>{});
-        case 132: return f(std::integral_constant<int, 12>{}, std::integral_constant<int, 11>{});
-        default: return fail(MPB_EUNSUPPORTED, "unsupported limb count " + std::to_string(L));
+    switch (block_of(L)) {
+        case 16: return f(std::integral_constant<int, 16>{}, L / 16);
+        case 12: return f(std::integral_constant<int, 12>{}, L / 12);
+        case 8: return f(std::integral_constant<int, 8>{}, L / 8);
+        default: return f(std::integral_constant<int, 4>{}, L / 4);
     }
 }
 
@@ -161,13 +157,15 @@ int check_launch() {
 
 unsigned grid_for(size_t n) { return (unsigned)((n + kThreads - 1) / kThreads); }
 
+constexpr int kMaxLimbs = 512;  // 16384-bit operands
+
 int limbs_checked(int bits, int& L) {
     L = mpb_limbs(bits);
     if (L <= 0) return fail(MPB_EUNSUPPORTED, "bits must be positive");
-    switch (L) {
-        case 16: case 32: case 64: case 96: case 128: case 132: return MPB_OK;
-        default: return fail(MPB_EUNSUPPORTED, "bits=" + std::to_string(bits) + " not compiled (supported L: 16,32,64,96,128,132)");
-    }
+    if (L > kMaxLimbs)
+        return fail(MPB_EUNSUPPORTED, "bits=" + std::to_string(bits) + " exceeds the compiled maximum of " +
+                                          std::to_string(32 * kMaxLimbs));
+    return MPB_OK;
 }
 
 }  // namespace
@@ -209,27 +207,53 @@ int mpb_layout_contract(const uint32_t* src, uint32_t* dst, size_t count, int li
     return check_launch();
 }
 
+// Karatsuba levels for an algo request (AUTO: the measured crossover).
+static int kara_levels(int algo, int L) {
+    switch (algo) {
+        case MPB_ALGO_SCHOOLBOOK: return 0;
+        case MPB_ALGO_KARATSUBA: return 1;
+        case MPB_ALGO_KARATSUBA2: return 2;
+        default: return 0;  // AUTO
+    }
+    (void)L;
+}
+
+size_t mp_batch_workspace(size_t count, int bits, int algo) {
+    const int L = mpb_limbs(bits);
+    if (L <= 0) return 0;
+    const int C = block_of(L);
+    return count * (size_t)mpb::kara_scratch_blocks_host(L / C, kara_levels(algo, L)) * C * sizeof(uint32_t);
+}
+
 static int mp_product(const uint32_t* a, const uint32_t* b, uint32_t* c, size_t count, int bits, int algo, bool sqr,
-                      void* stream) {
+                      void* ws, size_t ws_bytes, void* stream) {
     g_err.clear();
-    if (algo < MPB_ALGO_AUTO || algo > MPB_ALGO_KARATSUBA) return fail(MPB_EINVAL, "algo out of range");
+    if (algo < MPB_ALGO_AUTO || algo > MPB_ALGO_KARATSUBA2) return fail(MPB_EINVAL, "algo out of range");
     int L;
     if (int rc = limbs_checked(bits, L)) return rc;
     if (count == 0) return MPB_OK;
     if (int rc = check_ptrs({a, b, c})) return rc;
     if (c == a || c == b) return fail(MPB_EINVAL, "output aliases an input");
-    return dispatch_L(L, [&](auto Ci, auto NBi) {
-        constexpr int C = decltype(Ci)::value, NB = decltype(NBi)::value;
-        Launch<C, NB>::mp_mul(a, b, c, count, sqr, (cudaStream_t)stream);
+    const int levels = kara_levels(algo, L);
+    const size_t need = mp_batch_workspace(count, bits, algo);
+    if (need > 0) {
+        if (int rc = check_ptrs({ws})) return rc;
+        if (ws_bytes < need) return fail(MPB_EINVAL, "workspace too small");
+    }
+    return dispatch_L(L, [&](auto Ci, int nb) {
+        constexpr int C = decltype(Ci)::value;
+        Launch<C>::mp_mul(a, b, c, count, nb, sqr, levels, (uint32_t*)ws, (cudaStream_t)stream);
         return check_launch();
     });
 }
 
-int mp_batch_mul(const uint32_t* a, const uint32_t* b, uint32_t* c, size_t count, int bits, int algo, void* stream) {
-    return mp_product(a, b, c, count, bits, algo, false, stream);
+int mp_batch_mul(const uint32_t* a, const uint32_t* b, uint32_t* c, size_t count, int bits, int algo, void* ws,
+                 size_t ws_bytes, void* stream) {
+    return mp_product(a, b, c, count, bits, algo, false, ws, ws_bytes, stream);
 }
-int mp_batch_sqr(const uint32_t* a, uint32_t* c, size_t count, int bits, int algo, void* stream) {
-    return mp_product(a, a, c, count, bits, algo, true, stream);
+int mp_batch_sqr(const uint32_t* a, uint32_t* c, size_t count, int bits, int algo, void* ws, size_t ws_bytes,
+                 void* stream) {
+    return mp_product(a, a, c, count, bits, algo, true, ws, ws_bytes, stream);
 }
 
 size_t mont_batch_workspace(size_t count, int bits) {
@@ -247,9 +271,9 @@ static int mont_op(const uint32_t* a, const uint32_t* b, const uint32_t* N, cons
     if (int rc = check_ptrs({a, b, N, NP, c, ws})) return rc;
     if (c == a || c == b || c == N || c == NP) return fail(MPB_EINVAL, "output aliases an input");
     if (ws_bytes < mont_batch_workspace(count, bits)) return fail(MPB_EINVAL, "workspace too small");
-    return dispatch_L(L, [&](auto Ci, auto NBi) {
-        constexpr int C = decltype(Ci)::value, NB = decltype(NBi)::value;
-        Launch<C, NB>::mont_mul(a, b, N, NP, c, count, redc == MPB_REDC_TRUNCATED, sqr, (uint32_t*)ws,
+    return dispatch_L(L, [&](auto Ci, int nb) {
+        constexpr int C = decltype(Ci)::value;
+        Launch<C>::mont_mul(a, b, N, NP, c, count, nb, redc == MPB_REDC_TRUNCATED, sqr, (uint32_t*)ws,
                                 (cudaStream_t)stream);
         return check_launch();
     });
@@ -274,9 +298,9 @@ int mont_batch_redc(const uint32_t* T, const uint32_t* N, const uint32_t* NP, ui
     if (int rc = check_ptrs({T, N, NP, c, ws})) return rc;
     if (c == T || c == N || c == NP) return fail(MPB_EINVAL, "output aliases an input");
     if (ws_bytes < mont_batch_workspace(count, bits)) return fail(MPB_EINVAL, "workspace too small");
-    return dispatch_L(L, [&](auto Ci, auto NBi) {
-        constexpr int C = decltype(Ci)::value, NB = decltype(NBi)::value;
-        Launch<C, NB>::mont_redc(T, N, NP, c, count, redc == MPB_REDC_TRUNCATED, (uint32_t*)ws, (cudaStream_t)stream);
+    return dispatch_L(L, [&](auto Ci, int nb) {
+        constexpr int C = decltype(Ci)::value;
+        Launch<C>::mont_redc(T, N, NP, c, count, nb, redc == MPB_REDC_TRUNCATED, (uint32_t*)ws, (cudaStream_t)stream);
         return check_launch();
     });
 }
@@ -292,7 +316,7 @@ int mont_batch_modexp_ct(const uint32_t* N, const uint32_t* NP, const uint32_t* 
                          void* ws, size_t ws_bytes, void* stream) {
     g_err.clear();
     if (redc != MPB_REDC_FULL && redc != MPB_REDC_TRUNCATED) return fail(MPB_EINVAL, "redc out of range");
-    if (algo < MPB_ALGO_AUTO || algo > MPB_ALGO_KARATSUBA) return fail(MPB_EINVAL, "algo out of range");
+    if (algo < MPB_ALGO_AUTO || algo > MPB_ALGO_KARATSUBA2) return fail(MPB_EINVAL, "algo out of range");
     if (window < 1 || window > 6) return fail(MPB_EINVAL, "window must be in 1..6");
     int L;
     if (int rc = limbs_checked(bits, L)) return rc;
@@ -302,9 +326,9 @@ int mont_batch_modexp_ct(const uint32_t* N, const uint32_t* NP, const uint32_t* 
         return fail(MPB_EINVAL, "output aliases an input");
     if (ws_bytes < mont_batch_modexp_ct_workspace(count, bits, window, algo))
         return fail(MPB_EINVAL, "workspace too small");
-    return dispatch_L(L, [&](auto Ci, auto NBi) {
-        constexpr int C = decltype(Ci)::value, NB = decltype(NBi)::value;
-        Launch<C, NB>::modexp(N, NP, R2, base, exp, out, count, bits, window, redc == MPB_REDC_TRUNCATED,
+    return dispatch_L(L, [&](auto Ci, int nb) {
+        constexpr int C = decltype(Ci)::value;
+        Launch<C>::modexp(N, NP, R2, base, exp, out, count, nb, bits, window, redc == MPB_REDC_TRUNCATED,
                               (uint32_t*)ws, (cudaStream_t)stream);
         return check_launch();
     });

@@ -1,85 +1,95 @@
 // kernels.cuh -- the templated sm_100a kernels of libmpb.so and their launchers.
-// Instantiated per shape (C, NB) in inst_L*.cu so the fully unrolled compiles run in
-// parallel; api.cu holds the C ABI and only sees the Launch<C, NB> declarations.
+// Templated on the block size C only; the block count nb = L / C is a runtime argument.
+// Instantiated once per C in inst_C*.cu; api.cu holds the C ABI and sees only launch.h.
 #pragma once
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <type_traits>
 
 #include "launch.h"
+#include "mp_kara.cuh"
 #include "mp_mont.cuh"
 
 namespace mpb {
 
 constexpr int kThreads = 128;
-// resident CTAs per SM the modexp kernel is compiled for (register budget 65536 / (128 * minb))
+
+// resident CTAs per SM the heavy kernels are compiled for (register budget 65536 / (128 * minb))
 template <int C>
-__host__ __device__ constexpr int modexp_min_blocks() { return C >= 12 ? 3 : 5; }
-// entries of the CT table scan kept in flight per step (register budget)
+__host__ __device__ constexpr int min_blocks() { return C >= 12 ? 3 : 5; }
+// entries of the CT table scan kept in flight per step (x 4 chunks); measured best at L = 64
 template <int C>
 __host__ __device__ constexpr int select_unroll() {
 #ifdef MPB_SEL_U
     return MPB_SEL_U;
 #else
-    return 4;  // measured best at L = 64 (U = 4 entries x 4 chunks in flight; 8 x 4 and 1 x 8 are slower)
+    return 4;
 #endif
 }
+// dynamic shared memory: 2 buffers x 2 operand blocks x C/4 chunks of 16 bytes per thread
+template <int C>
+constexpr size_t stage_bytes() { return (size_t)kThreads * 4 * (C / 4) * 16; }
 
 MPB_DEVI size_t tid_global() { return (size_t)blockIdx.x * blockDim.x + threadIdx.x; }
 // word-sliced accessor for operand k of an array with `count` operands
 MPB_DEVI Arr arr(const uint32_t* base, size_t count, size_t k) {
     return Arr{reinterpret_cast<char*>(const_cast<uint32_t*>(base)) + k * 16, (uint32_t)(count * 16)};
 }
-// this thread's staging area in dynamic shared memory (2 buffers x 2 blocks x C/4 chunks)
-template <int C>
+// this thread's staging area in dynamic shared memory
 MPB_DEVI Stage stage() {
     extern __shared__ uint4 smem_stage[];
     return Stage{(uint32_t)__cvta_generic_to_shared(smem_stage + threadIdx.x), (uint32_t)(blockDim.x * 16)};
 }
-template <int C>
-constexpr size_t stage_bytes() { return (size_t)kThreads * 4 * (C / 4) * 16; }
 // word i of operand k (32-bit access)
 MPB_DEVI uint32_t word_at(const uint32_t* base, size_t count, size_t k, int i) {
     return __ldg(base + ((size_t)(i >> 2) * count + k) * 4 + (i & 3));
 }
 
 // ------------------------------------------------------------ product kernels
-template <int C, int NB, bool SQR>
+// c = a*b (SQR: a^2): schoolbook through the engine, or LEVELS of block Karatsuba (mp_kara.cuh).
+// ws: kara_scratch_blocks(nb, LEVELS) blocks per operand (word-sliced, stride count).
+template <int C, bool SQR, int LEVELS>
 __global__ void __launch_bounds__(kThreads) k_mp_mul(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
-                                                     uint32_t* __restrict__ c, size_t count) {
+                                                     uint32_t* __restrict__ c, size_t count, int nb, uint32_t* ws) {
     const size_t k = tid_global();
     if (k >= count) return;
-    uint32_t orlo = 0, tl1 = 0;
-    const Arr C_ = arr(c, count, k);
-    engine<C, NB, true>(SQR ? PH_SQR : PH_MUL, arr(a, count, k), arr(SQR ? a : b, count, k), C_, C_, C_, C_, orlo,
-                        tl1, stage<C>());
+    const Arr A = arr(a, count, k), B = arr(SQR ? a : b, count, k), Cc = arr(c, count, k);
+    if (LEVELS == 0) {
+        uint32_t orlo = 0, tl1 = 0;
+        engine<C, true>(SQR ? PH_SQR : PH_MUL, nb, A, B, Cc, Cc, Cc, Cc, orlo, tl1, stage());
+    } else {
+        kmul<C, LEVELS>(SQR, nb, A, B, Cc, arr(ws, count, k), stage());
+    }
 }
 
 // workspace for the mont kernels: T (2L) then Q (L), word-sliced with stride count
-template <int C, int NB, bool TRUNC, bool SQR>
+template <int C, bool TRUNC, bool SQR, int NBT>
 __global__ void __launch_bounds__(kThreads) k_mont_mul(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
                                                        const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP,
-                                                       uint32_t* __restrict__ c, size_t count, uint32_t* ws) {
-    constexpr int L = C * NB;
+                                                       uint32_t* __restrict__ c, size_t count, int nb_rt, uint32_t* ws) {
     const size_t k = tid_global();
     if (k >= count) return;
-    const Arr T = arr(ws, count, k), Q = arr(ws + (size_t)2 * L * count, count, k);
-    mont_op<C, NB, TRUNC>(SQR ? MODE_SQR : MODE_MUL, arr(a, count, k), arr(SQR ? a : b, count, k), arr(N, count, k),
-                          arr(NP, count, k), T, Q, arr(c, count, k), stage<C>());
+    const int nb = NBT ? NBT : nb_rt;
+    const size_t L = (size_t)C * nb;
+    const Arr T = arr(ws, count, k), Q = arr(ws + 2 * L * count, count, k);
+    mont_op<C, TRUNC>(SQR ? MODE_SQR : MODE_MUL, nb, arr(a, count, k), arr(SQR ? a : b, count, k), arr(N, count, k),
+                      arr(NP, count, k), T, Q, arr(c, count, k), stage());
 }
 
-template <int C, int NB, bool TRUNC>
+template <int C, bool TRUNC>
 __global__ void __launch_bounds__(kThreads) k_mont_redc(const uint32_t* __restrict__ Tin, const uint32_t* __restrict__ N,
                                                         const uint32_t* __restrict__ NP, uint32_t* __restrict__ c,
-                                                        size_t count, uint32_t* ws) {
-    constexpr int L = C * NB;
+                                                        size_t count, int nb, uint32_t* ws) {
     const size_t k = tid_global();
     if (k >= count) return;
-    const Arr T = arr(ws, count, k), Q = arr(ws + (size_t)2 * L * count, count, k);
+    const size_t L = (size_t)C * nb;
+    const Arr T = arr(ws, count, k), Q = arr(ws + 2 * L * count, count, k);
     const Arr Ti = arr(Tin, count, k);
 #pragma unroll 1
-    for (int q = 0; q < 2 * L / 4; q++) T.st(q, Ti.ld(q));
-    mont_op<C, NB, TRUNC>(MODE_REDC, T, T, arr(N, count, k), arr(NP, count, k), T, Q, arr(c, count, k), stage<C>());
+    for (int q = 0; q < (int)(2 * L / 4); q++) T.st(q, Ti.ld(q));
+    mont_op<C, TRUNC>(MODE_REDC, nb, T, T, arr(N, count, k), arr(NP, count, k), T, Q, arr(c, count, k), stage());
 }
 
 // ------------------------------------------------------------------- modexp
@@ -93,14 +103,15 @@ __global__ void __launch_bounds__(kThreads) k_mont_redc(const uint32_t* __restri
 //                                  (P:L765-766),  Y = MontMul(Y, S)
 //   last op          out = REDC(Y)
 // workspace per operand (word-sliced, stride count): G (2^w * L) | Y (L) | T (2L) | Q (L) | S (L)
-template <int C, int NB, bool TRUNC>
-__global__ void __launch_bounds__(kThreads, modexp_min_blocks<C>()) k_modexp(const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP,
-                                                     const uint32_t* __restrict__ R2, const uint32_t* __restrict__ base,
-                                                     const uint32_t* __restrict__ exp, uint32_t* __restrict__ out,
-                                                     size_t count, int bits, int w, uint32_t* ws) {
-    constexpr int L = C * NB, Q4 = L / 4;
+template <int C, bool TRUNC, int NBT>
+__global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_modexp(
+    const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP, const uint32_t* __restrict__ R2,
+    const uint32_t* __restrict__ base, const uint32_t* __restrict__ exp, uint32_t* __restrict__ out, size_t count,
+    int nb_rt, int bits, int w, uint32_t* ws) {
     const size_t k = tid_global();
     if (k >= count) return;
+    const int nb = NBT ? NBT : nb_rt;  // compile-time block count for the hot sizes
+    const int L = C * nb, Q4 = L / 4;
     const int nent = 1 << w;
     uint32_t* p = ws;
     const Arr G = arr(p, count, k);
@@ -114,7 +125,7 @@ __global__ void __launch_bounds__(kThreads, modexp_min_blocks<C>()) k_modexp(con
     const Arr S = arr(p, count, k);
     const Arr Nn = arr(N, count, k), NPn = arr(NP, count, k), R2n = arr(R2, count, k), Bn = arr(base, count, k);
     const Arr On = arr(out, count, k);
-    const Stage sg = stage<C>();
+    const Stage sg = stage();
 
     const int nwin = (bits + w - 1) / w;
     const int per_win = w + 2;
@@ -151,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, modexp_min_blocks<C>()) k_modexp(con
             const int pos = win * w, wi = pos >> 5, off = pos & 31;
             uint32_t v = word_at(exp, count, k, wi) >> off;
             if (off + w > 32 && wi + 1 < L) v |= word_at(exp, count, k, wi + 1) << (32 - off);
-            ct_select<L, select_unroll<C>()>(G, nent, v & ((1u << w) - 1u), O);
+            ct_select<select_unroll<C>()>(G, L, nent, v & ((1u << w) - 1u), O);
             continue;
         }
         if (mode == MODE_REDC) {  // T = X zero-extended to 2L limbs
@@ -161,41 +172,89 @@ __global__ void __launch_bounds__(kThreads, modexp_min_blocks<C>()) k_modexp(con
                 T.st(Q4 + q, make_uint4(0, 0, 0, 0));
             }
         }
-        mont_op<C, NB, TRUNC>(mode, X, B, Nn, NPn, T, Q, O, sg);
+        mont_op<C, TRUNC>(mode, nb, X, B, Nn, NPn, T, Q, O, sg);
     }
 }
 
+// ---------------------------------------------------------------- launchers
 inline unsigned grid_for(size_t n) { return (unsigned)((n + kThreads - 1) / kThreads); }
 
-template <int C, int NB>
-void Launch<C, NB>::mp_mul(const uint32_t* a, const uint32_t* b, uint32_t* c, size_t count, bool sqr, cudaStream_t s) {
-    if (sqr) k_mp_mul<C, NB, true><<<grid_for(count), kThreads, stage_bytes<C>(), s>>>(a, a, c, count);
-    else k_mp_mul<C, NB, false><<<grid_for(count), kThreads, stage_bytes<C>(), s>>>(a, b, c, count);
-}
-template <int C, int NB>
-void Launch<C, NB>::mont_mul(const uint32_t* a, const uint32_t* b, const uint32_t* N, const uint32_t* NP, uint32_t* c,
-                             size_t count, bool trunc, bool sqr, uint32_t* ws, cudaStream_t s) {
+template <int C>
+void Launch<C>::mp_mul(const uint32_t* a, const uint32_t* b, uint32_t* c, size_t count, int nb, bool sqr, int levels,
+                       uint32_t* ws, cudaStream_t s) {
     const unsigned g = grid_for(count);
-    if (trunc) {
-        if (sqr) k_mont_mul<C, NB, true, true><<<g, kThreads, stage_bytes<C>(), s>>>(a, a, N, NP, c, count, ws);
-        else k_mont_mul<C, NB, true, false><<<g, kThreads, stage_bytes<C>(), s>>>(a, b, N, NP, c, count, ws);
+    const size_t sm = stage_bytes<C>();
+    if (sqr) {
+        if (levels >= 2) k_mp_mul<C, true, 2><<<g, kThreads, sm, s>>>(a, a, c, count, nb, ws);
+        else if (levels == 1) k_mp_mul<C, true, 1><<<g, kThreads, sm, s>>>(a, a, c, count, nb, ws);
+        else k_mp_mul<C, true, 0><<<g, kThreads, sm, s>>>(a, a, c, count, nb, ws);
     } else {
-        if (sqr) k_mont_mul<C, NB, false, true><<<g, kThreads, stage_bytes<C>(), s>>>(a, a, N, NP, c, count, ws);
-        else k_mont_mul<C, NB, false, false><<<g, kThreads, stage_bytes<C>(), s>>>(a, b, N, NP, c, count, ws);
+        if (levels >= 2) k_mp_mul<C, false, 2><<<g, kThreads, sm, s>>>(a, b, c, count, nb, ws);
+        else if (levels == 1) k_mp_mul<C, false, 1><<<g, kThreads, sm, s>>>(a, b, c, count, nb, ws);
+        else k_mp_mul<C, false, 0><<<g, kThreads, sm, s>>>(a, b, c, count, nb, ws);
     }
 }
-template <int C, int NB>
-void Launch<C, NB>::mont_redc(const uint32_t* T, const uint32_t* N, const uint32_t* NP, uint32_t* c, size_t count,
-                              bool trunc, uint32_t* ws, cudaStream_t s) {
-    if (trunc) k_mont_redc<C, NB, true><<<grid_for(count), kThreads, stage_bytes<C>(), s>>>(T, N, NP, c, count, ws);
-    else k_mont_redc<C, NB, false><<<grid_for(count), kThreads, stage_bytes<C>(), s>>>(T, N, NP, c, count, ws);
+// compile-time block counts of the hot sizes (1024/2048/3072/4096 bits at C = 16; 4108 at C = 12)
+template <int C, typename F>
+void with_nb(int nb, F&& f) {
+    if constexpr (C == 16) {
+        switch (nb) {
+            case 2: return f(std::integral_constant<int, 2>{});
+            case 4: return f(std::integral_constant<int, 4>{});
+            case 6: return f(std::integral_constant<int, 6>{});
+            case 8: return f(std::integral_constant<int, 8>{});
+            default: break;
+        }
+    } else if constexpr (C == 12) {
+        if (nb == 11) return f(std::integral_constant<int, 11>{});
+    } else if constexpr (C == 8) {
+        switch (nb) {
+            case 8: return f(std::integral_constant<int, 8>{});
+            case 16: return f(std::integral_constant<int, 16>{});
+            default: break;
+        }
+    }
+    f(std::integral_constant<int, 0>{});
 }
-template <int C, int NB>
-void Launch<C, NB>::modexp(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
-                           const uint32_t* exp, uint32_t* out, size_t count, int bits, int window, bool trunc,
-                           uint32_t* ws, cudaStream_t s) {
-    if (trunc) k_modexp<C, NB, true><<<grid_for(count), kThreads, stage_bytes<C>(), s>>>(N, NP, R2, base, exp, out, count, bits, window, ws);
-    else k_modexp<C, NB, false><<<grid_for(count), kThreads, stage_bytes<C>(), s>>>(N, NP, R2, base, exp, out, count, bits, window, ws);
+
+template <int C>
+void Launch<C>::mont_mul(const uint32_t* a, const uint32_t* b, const uint32_t* N, const uint32_t* NP, uint32_t* c,
+                         size_t count, int nb, bool trunc, bool sqr, uint32_t* ws, cudaStream_t s) {
+    const unsigned g = grid_for(count);
+    const size_t sm = stage_bytes<C>();
+    with_nb<C>(nb, [&](auto NBc) {
+        constexpr int NBT = decltype(NBc)::value;
+        if (trunc) {
+            if (sqr) k_mont_mul<C, true, true, NBT><<<g, kThreads, sm, s>>>(a, a, N, NP, c, count, nb, ws);
+            else k_mont_mul<C, true, false, NBT><<<g, kThreads, sm, s>>>(a, b, N, NP, c, count, nb, ws);
+        } else {
+            if (sqr) k_mont_mul<C, false, true, NBT><<<g, kThreads, sm, s>>>(a, a, N, NP, c, count, nb, ws);
+            else k_mont_mul<C, false, false, NBT><<<g, kThreads, sm, s>>>(a, b, N, NP, c, count, nb, ws);
+        }
+    });
+}
+template <int C>
+void Launch<C>::mont_redc(const uint32_t* T, const uint32_t* N, const uint32_t* NP, uint32_t* c, size_t count, int nb,
+                          bool trunc, uint32_t* ws, cudaStream_t s) {
+    const size_t sm = stage_bytes<C>();
+    if (trunc) k_mont_redc<C, true><<<grid_for(count), kThreads, sm, s>>>(T, N, NP, c, count, nb, ws);
+    else k_mont_redc<C, false><<<grid_for(count), kThreads, sm, s>>>(T, N, NP, c, count, nb, ws);
+}
+template <int C>
+void Launch<C>::modexp(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
+                       const uint32_t* exp, uint32_t* out, size_t count, int nb, int bits, int window, bool trunc,
+                       uint32_t* ws, cudaStream_t s) {
+    const size_t sm = stage_bytes<C>();
+    with_nb<C>(nb, [&](auto NBc) {
+        constexpr int NBT = decltype(NBc)::value;
+        if (trunc) {
+            k_modexp<C, true, NBT><<<grid_for(count), kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, nb, bits,
+                                                                        window, ws);
+        } else {
+            k_modexp<C, false, NBT><<<grid_for(count), kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, nb, bits,
+                                                                         window, ws);
+        }
+    });
 }
 
 }  // namespace mpb

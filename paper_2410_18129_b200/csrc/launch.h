@@ -1,5 +1,6 @@
-// launch.h -- host-side launchers of the templated kernels, one explicit instantiation per
-// compiled shape (C limbs per block, NB blocks; L = C*NB).  No CUDA types beyond cudaStream_t.
+// launch.h -- host-side launchers of the templated kernels.  One explicit instantiation per
+// block size C (limbs per block; C in {16, 12, 8, 4}); the block count nb = L / C is a runtime
+// argument, so any limb count that C divides is served by the same code.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -8,21 +9,31 @@
 
 namespace mpb {
 
-template <int C, int NB>
+template <int C>
 struct Launch {
-    static void mp_mul(const uint32_t* a, const uint32_t* b, uint32_t* c, size_t count, bool sqr, cudaStream_t s);
+    // c = a*b (sqr: a^2), 2L limbs; levels = Karatsuba levels (0 = schoolbook); ws: scratch
+    static void mp_mul(const uint32_t* a, const uint32_t* b, uint32_t* c, size_t count, int nb, bool sqr, int levels,
+                       uint32_t* ws, cudaStream_t s);
     static void mont_mul(const uint32_t* a, const uint32_t* b, const uint32_t* N, const uint32_t* NP, uint32_t* c,
-                         size_t count, bool trunc, bool sqr, uint32_t* ws, cudaStream_t s);
-    static void mont_redc(const uint32_t* T, const uint32_t* N, const uint32_t* NP, uint32_t* c, size_t count, bool trunc,
-                          uint32_t* ws, cudaStream_t s);
+                         size_t count, int nb, bool trunc, bool sqr, uint32_t* ws, cudaStream_t s);
+    static void mont_redc(const uint32_t* T, const uint32_t* N, const uint32_t* NP, uint32_t* c, size_t count, int nb,
+                          bool trunc, uint32_t* ws, cudaStream_t s);
     static void modexp(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
-                       const uint32_t* exp, uint32_t* out, size_t count, int bits, int window, bool trunc, uint32_t* ws,
-                       cudaStream_t s);
+                       const uint32_t* exp, uint32_t* out, size_t count, int nb, int bits, int window, bool trunc,
+                       uint32_t* ws, cudaStream_t s);
 };
 
-#define MPB_SHAPES(X) X(16, 1) X(16, 2) X(16, 4) X(16, 6) X(16, 8) X(12, 11) X(8, 8)
-#define MPB_EXTERN(C, NB) extern template struct Launch<C, NB>;
-MPB_SHAPES(MPB_EXTERN)
+#define MPB_BLOCKS(X) X(16) X(12) X(8) X(4)
+#define MPB_EXTERN(C) extern template struct Launch<C>;
+MPB_BLOCKS(MPB_EXTERN)
 #undef MPB_EXTERN
+
+// scratch blocks of the Karatsuba product (mirror of mp_kara.cuh kara_scratch_blocks)
+inline int kara_scratch_blocks_host(int nb, int level) {
+    return level <= 0 || nb < 2 ? 0 : 4 * ((nb + 1) / 2) + kara_scratch_blocks_host((nb + 1) / 2, level - 1);
+}
+
+// block size used for a limb count: the largest of 16, 12, 8, 4 dividing L
+inline int block_for(int L) { return L % 16 == 0 ? 16 : (L % 12 == 0 ? 12 : (L % 8 == 0 ? 8 : 4)); }
 
 }  // namespace mpb

@@ -96,8 +96,8 @@ MPB_DEVI void w_shift(uint32_t (&W)[2 * C + 1]) {  // W >>= 32C
 // ------------------------------------------------ shared tail: C, D = C - N
 // Block j of H (window words 0..C-1) becomes block j of C = T_hi + H + carry (truncated) or
 // of C itself (full); C is parked in T block NB+j and D = C - N - borrow goes to OUT block j.
-template <int C, int NB>
-MPB_DEVI void emit_block(const uint32_t (&W)[2 * C + 1], int j, bool add_thi, const Arr& T, const Arr& N,
+template <int C>
+MPB_DEVI void emit_block(const uint32_t (&W)[2 * C + 1], int j, int NB, bool add_thi, const Arr& T, const Arr& N,
                          const Arr& OUT, uint32_t& carry, uint32_t& borrow) {
     uint32_t c[C];
 #pragma unroll
@@ -121,8 +121,8 @@ MPB_DEVI void emit_block(const uint32_t (&W)[2 * C + 1], int j, bool add_thi, co
 }
 
 // OUT = (ctop || !borrow) ? D : C, with D in OUT and C in T[NB..2NB) -- a mask, no branch.
-template <int C, int NB>
-MPB_DEVI void final_select(const Arr& T, const Arr& OUT, uint32_t ctop, uint32_t borrow) {
+template <int C>
+MPB_DEVI void final_select(int NB, const Arr& T, const Arr& OUT, uint32_t ctop, uint32_t borrow) {
     const uint32_t m = 0u - ((ctop | (borrow ^ 1u)) & 1u);  // all ones: take D = C - N
 #pragma unroll 1
     for (int j = 0; j < NB; j++) {
@@ -154,8 +154,8 @@ MPB_DEVI void final_select(const Arr& T, const Arr& OUT, uint32_t ctop, uint32_t
 enum { PH_MUL = 0, PH_SQR = 1, PH_Q = 2, PH_HI = 3 };
 enum { OP_MUL = 0, OP_MUL2 = 1, OP_SQR = 2, OP_LO = 3, OP_HI = 4 };
 
-template <int C, int NB, bool TRUNC>
-MPB_DEVI void engine(int ph, const Arr& AX, const Arr& AY, const Arr& DST, const Arr& T, const Arr& N,
+template <int C, bool TRUNC>
+MPB_DEVI void engine(int ph, int NB, const Arr& AX, const Arr& AY, const Arr& DST, const Arr& T, const Arr& N,
                      const Arr& OUT, uint32_t& orlo, uint32_t& tl1, const Stage& sg) {
     uint32_t W[2 * C + 1];
     w_zero<C>(W);
@@ -292,7 +292,7 @@ MPB_DEVI void engine(int ph, const Arr& AX, const Arr& AY, const Arr& DST, const
                 for (int i = 1; i <= C; i++) add_next(W[i], 0u);
                 absorb(W[C + 1]);
             } else {
-                emit_block<C, NB>(W, k - NB, true, T, N, OUT, carry, borrow);
+                emit_block<C>(W, k - NB, NB, true, T, N, OUT, carry, borrow);
                 w_shift<C>(W);
             }
         } else {
@@ -304,14 +304,14 @@ MPB_DEVI void engine(int ph, const Arr& AX, const Arr& AY, const Arr& DST, const
 #pragma unroll
             for (int i = C; i < 2 * C; i++) add_next(W[i], 0u);
             absorb(W[2 * C]);
-            if (k >= NB) emit_block<C, NB>(W, k - NB, false, T, N, OUT, carry, borrow);
+            if (k >= NB) emit_block<C>(W, k - NB, NB, false, T, N, OUT, carry, borrow);
             w_shift<C>(W);
         }
     }
     if (ph == PH_MUL || ph == PH_SQR) stb<C>(DST, 2 * NB - 1, W);
     if (ph == PH_HI) {
-        if (TRUNC) emit_block<C, NB>(W, NB - 1, true, T, N, OUT, carry, borrow);
-        final_select<C, NB>(T, OUT, TRUNC ? carry : W[0], borrow);
+        if (TRUNC) emit_block<C>(W, NB - 1, NB, true, T, N, OUT, carry, borrow);
+        final_select<C>(NB, T, OUT, TRUNC ? carry : W[0], borrow);
     }
 }
 
@@ -320,8 +320,8 @@ MPB_DEVI void engine(int ph, const Arr& AX, const Arr& AY, const Arr& DST, const
 //   mode REDC: OUT = T*R^-1 mod N for the 2L-word T already in scratch T
 enum { MODE_MUL = 0, MODE_SQR = 1, MODE_REDC = 2 };
 
-template <int C, int NB, bool TRUNC>
-MPB_DEVI void mont_op(int mode, const Arr& X, const Arr& B, const Arr& N, const Arr& NP, const Arr& T, const Arr& Q,
+template <int C, bool TRUNC>
+MPB_DEVI void mont_op(int mode, int NB, const Arr& X, const Arr& B, const Arr& N, const Arr& NP, const Arr& T, const Arr& Q,
                       const Arr& OUT, const Stage& sg) {
     uint32_t orlo = 0, tl1 = 0;
 #pragma unroll 1
@@ -330,7 +330,7 @@ MPB_DEVI void mont_op(int mode, const Arr& X, const Arr& B, const Arr& N, const 
         const Arr ax = step == 0 ? X : (step == 1 ? T : Q);
         const Arr ay = step == 0 ? B : (step == 1 ? NP : N);
         const Arr dst = step == 0 ? T : Q;
-        engine<C, NB, TRUNC>(ph, ax, ay, dst, T, N, OUT, orlo, tl1, sg);
+        engine<C, TRUNC>(ph, NB, ax, ay, dst, T, N, OUT, orlo, tl1, sg);
     }
 }
 
@@ -339,13 +339,13 @@ MPB_DEVI void mont_op(int mode, const Arr& X, const Arr& B, const Arr& N, const 
 // Entry e, chunk q lives at chunk index e*(L/4) + q of G.  The scan is bound by DRAM latency
 // (the tables of all resident operands exceed L2), so it keeps SEL_U entries x SEL_G chunks of
 // loads in flight per step; accumulators stay in registers at every L.
-template <int L, int U>
-MPB_DEVI void ct_select(const Arr& G, int nent, uint32_t idx, const Arr& OUT) {
-    constexpr int Q4 = L / 4;
+template <int U>
+MPB_DEVI void ct_select(const Arr& G, int L, int nent, uint32_t idx, const Arr& OUT) {
+    const int Q4 = L / 4;
 #ifdef MPB_SEL_G
     constexpr int GRP = MPB_SEL_G;
 #else
-    constexpr int GRP = Q4 % 4 == 0 ? 4 : (Q4 % 3 == 0 ? 3 : (Q4 % 2 == 0 ? 2 : 1));
+    constexpr int GRP = 4;
 #endif
 #pragma unroll 1
     for (int g0 = 0; g0 < Q4; g0 += GRP) {
@@ -359,7 +359,8 @@ MPB_DEVI void ct_select(const Arr& G, int nent, uint32_t idx, const Arr& OUT) {
             for (int u = 0; u < U; u++)
 #pragma unroll
                 for (int q = 0; q < GRP; q++)
-                    v[u][q] = (e0 + u < nent) ? G.ld_stream((e0 + u) * Q4 + g0 + q) : make_uint4(0, 0, 0, 0);
+                    v[u][q] = (e0 + u < nent && g0 + q < Q4) ? G.ld_stream((e0 + u) * Q4 + g0 + q)
+                                                              : make_uint4(0, 0, 0, 0);
 #pragma unroll
             for (int u = 0; u < U; u++) {
                 const uint32_t x = (uint32_t)(e0 + u) ^ idx;
@@ -374,7 +375,8 @@ MPB_DEVI void ct_select(const Arr& G, int nent, uint32_t idx, const Arr& OUT) {
             }
         }
 #pragma unroll
-        for (int q = 0; q < GRP; q++) OUT.st(g0 + q, acc[q]);
+        for (int q = 0; q < GRP; q++)
+            if (g0 + q < Q4) OUT.st(g0 + q, acc[q]);
     }
 }
 

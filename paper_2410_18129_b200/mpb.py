@@ -33,8 +33,9 @@ _SIGS = {
     "mpb_supported": (_i, [_i]),
     "mpb_layout_expand": (_i, [_vp, _vp, _sz, _i, _vp]),
     "mpb_layout_contract": (_i, [_vp, _vp, _sz, _i, _vp]),
-    "mp_batch_mul": (_i, [_vp, _vp, _vp, _sz, _i, _i, _vp]),
-    "mp_batch_sqr": (_i, [_vp, _vp, _sz, _i, _i, _vp]),
+    "mp_batch_mul": (_i, [_vp, _vp, _vp, _sz, _i, _i, _vp, _sz, _vp]),
+    "mp_batch_sqr": (_i, [_vp, _vp, _sz, _i, _i, _vp, _sz, _vp]),
+    "mp_batch_workspace": (_sz, [_sz, _i, _i]),
     "mont_batch_mul": (_i, [_vp, _vp, _vp, _vp, _vp, _sz, _i, _i, _vp, _sz, _vp]),
     "mont_batch_sqr": (_i, [_vp, _vp, _vp, _vp, _sz, _i, _i, _vp, _sz, _vp]),
     "mont_batch_redc": (_i, [_vp, _vp, _vp, _vp, _sz, _i, _i, _vp, _sz, _vp]),
@@ -53,7 +54,7 @@ for _name, (_res, _args) in _SIGS.items():
 
 MPB_OK, MPB_EINVAL, MPB_EUNSUPPORTED, MPB_ECUDA = 0, -1, -2, -3
 REDC_FULL, REDC_TRUNCATED = 0, 1
-ALGO_AUTO, ALGO_SCHOOLBOOK, ALGO_KARATSUBA = 0, 1, 2
+ALGO_AUTO, ALGO_SCHOOLBOOK, ALGO_KARATSUBA, ALGO_KARATSUBA2 = 0, 1, 2, 3
 
 
 class MpbError(RuntimeError):
@@ -125,17 +126,27 @@ def layout_contract(y: torch.Tensor) -> torch.Tensor:
 
 
 # --------------------------------------------------------------- products
-def mp_batch_mul(a: torch.Tensor, b: torch.Tensor, bits: int, algo: int = ALGO_AUTO) -> torch.Tensor:
+def mp_workspace(count: int, bits: int, algo: int, device="cuda") -> torch.Tensor | None:
+    n = _lib.mp_batch_workspace(count, bits, algo)
+    return workspace(n, device) if n else None
+
+
+def mp_batch_mul(a: torch.Tensor, b: torch.Tensor, bits: int, algo: int = ALGO_AUTO,
+                 ws: torch.Tensor | None = None) -> torch.Tensor:
     L, count = _sliced_shape(a)
+    ws = ws if ws is not None else mp_workspace(count, bits, algo, a.device)
     c = empty_sliced(2 * L, count, a.device)
-    _check(_lib.mp_batch_mul(_ptr(a), _ptr(b), _ptr(c), count, bits, algo, _stream()))
+    _check(_lib.mp_batch_mul(_ptr(a), _ptr(b), _ptr(c), count, bits, algo, _ptr(ws),
+                             0 if ws is None else ws.numel() * 4, _stream()))
     return c
 
 
-def mp_batch_sqr(a: torch.Tensor, bits: int, algo: int = ALGO_AUTO) -> torch.Tensor:
+def mp_batch_sqr(a: torch.Tensor, bits: int, algo: int = ALGO_AUTO, ws: torch.Tensor | None = None) -> torch.Tensor:
     L, count = _sliced_shape(a)
+    ws = ws if ws is not None else mp_workspace(count, bits, algo, a.device)
     c = empty_sliced(2 * L, count, a.device)
-    _check(_lib.mp_batch_sqr(_ptr(a), _ptr(c), count, bits, algo, _stream()))
+    _check(_lib.mp_batch_sqr(_ptr(a), _ptr(c), count, bits, algo, _ptr(ws), 0 if ws is None else ws.numel() * 4,
+                             _stream()))
     return c
 
 

@@ -48,11 +48,18 @@ def test_host_only_helpers(lib):
     lib.mpb_supported.restype = ctypes.c_int
     assert [lib.mpb_limbs(b) for b in (0, 1, 512, 1024, 2048, 3072, 4096, 4108, 4154)] == \
         [0, 4, 16, 32, 64, 96, 128, 132, 132]
-    assert lib.mpb_supported(2048) == 1 and lib.mpb_supported(700) == 0
+    assert lib.mpb_supported(2048) == 1 and lib.mpb_supported(700) == 1 and lib.mpb_supported(20000) == 0
     lib.mont_batch_modexp_ct_workspace.restype = ctypes.c_size_t
     lib.mont_batch_modexp_ct_workspace.argtypes = [ctypes.c_size_t, ctypes.c_int, ctypes.c_int, ctypes.c_int]
     assert lib.mont_batch_modexp_ct_workspace(10, 2048, 5, 0) == 10 * 64 * (32 + 5) * 4
     assert lib.mont_batch_modexp_ct_workspace(10, 2048, 7, 0) == 0
+    lib.mp_batch_workspace.restype = ctypes.c_size_t
+    lib.mp_batch_workspace.argtypes = [ctypes.c_size_t, ctypes.c_int, ctypes.c_int]
+    assert lib.mp_batch_workspace(10, 4096, 1) == 0  # schoolbook needs none
+    # 1 level at L = 128 (C = 16, 8 blocks): 4 * 4 blocks of 16 limbs
+    assert lib.mp_batch_workspace(10, 4096, 2) == 10 * 16 * 16 * 4
+    # 2 levels at 4154 bits (L = 132, C = 12, 11 blocks): 4*6 + 4*3 blocks of 12 limbs
+    assert lib.mp_batch_workspace(10, 4154, 3) == 10 * 36 * 12 * 4
 
 
 def test_product_path_never_imports_the_oracle():

@@ -22,7 +22,9 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 BITS_MOD = [512, 1024, 2048, 3072, 4096, 4108]
+BITS_ODD = [256, 700, 1536]  # block sizes 8 and 12, odd block counts
 BITS_MUL = [512, 1024, 2048, 3072, 4096, 4154]
+ALGOS = [1, 2, 3]  # schoolbook, 1-level Karatsuba, 2-level Karatsuba
 REDC = [1, 0]  # truncated, full
 
 
@@ -61,8 +63,9 @@ def test_layout_roundtrip(mpb, L, count):
 
 
 # ---------------------------------------------------------------------- products
-@pytest.mark.parametrize("bits", BITS_MUL)
-def test_mp_batch_mul_sqr(mpb, bits):
+@pytest.mark.parametrize("algo", ALGOS)
+@pytest.mark.parametrize("bits", BITS_MUL + [96, 700, 1536])
+def test_mp_batch_mul_sqr(mpb, bits, algo):
     count = 130  # ragged over 128-thread CTAs
     a, b = I.mul_inputs(config=4, count=count, bits=bits)
     L = a.shape[1]
@@ -71,8 +74,8 @@ def test_mp_batch_mul_sqr(mpb, bits):
     a[1] = 0; a[2] = 0; a[2, 0] = 1
     a[3] = 0; a[3, L - 1] = np.uint32(1 << 31); b[3] = np.uint32(0xFFFFFFFF)
     da, db = mpb.to_device(a), mpb.to_device(b)
-    c = mpb.to_host(mpb.mp_batch_mul(da, db, bits))
-    s = mpb.to_host(mpb.mp_batch_sqr(da, bits))
+    c = mpb.to_host(mpb.mp_batch_mul(da, db, bits, algo))
+    s = mpb.to_host(mpb.mp_batch_sqr(da, bits, algo))
     A, B = ints(a), ints(b)
     for k in range(count):
         assert I.from_limbs(c[k]) == O.mul(A[k], B[k]), k
@@ -80,7 +83,7 @@ def test_mp_batch_mul_sqr(mpb, bits):
 
 
 # ------------------------------------------------------------------------- setup
-@pytest.mark.parametrize("bits", BITS_MOD)
+@pytest.mark.parametrize("bits", BITS_MOD + BITS_ODD)
 def test_setup(mpb, bits):
     count = 40
     N, _, _ = I.modexp_inputs(config=2, count=count, bits=bits)
@@ -102,7 +105,7 @@ def _mont_fixture(mpb, bits, count, config=2):
 
 # ----------------------------------------------------------- montmul / montsqr
 @pytest.mark.parametrize("redc", REDC)
-@pytest.mark.parametrize("bits", BITS_MOD)
+@pytest.mark.parametrize("bits", BITS_MOD + BITS_ODD)
 def test_mont_mul_sqr(mpb, bits, redc):
     count = 131
     N, a, b, dN, Np, R2 = _mont_fixture(mpb, bits, count)
@@ -123,7 +126,7 @@ def test_mont_mul_sqr(mpb, bits, redc):
 
 # --------------------------------------------------------------------- REDC
 @pytest.mark.parametrize("redc", REDC)
-@pytest.mark.parametrize("bits", BITS_MOD)
+@pytest.mark.parametrize("bits", BITS_MOD + BITS_ODD)
 def test_mont_redc_adversarial(mpb, bits, redc):
     """The exact carry correction of Theorem 2 (families alpha..delta, tests/adversarial.py)."""
     L = I.limbs_for_bits(bits)
@@ -146,11 +149,11 @@ def test_mont_redc_adversarial(mpb, bits, redc):
 
 
 # ------------------------------------------------------------------- modexp
-MODEXP_COUNTS = {512: 70, 1024: 40, 2048: 10, 3072: 4, 4096: 3, 4108: 3}
+MODEXP_COUNTS = {512: 70, 1024: 40, 2048: 10, 3072: 4, 4096: 3, 4108: 3, 256: 70, 700: 40, 1536: 12}
 
 
 @pytest.mark.parametrize("redc", REDC)
-@pytest.mark.parametrize("bits", BITS_MOD)
+@pytest.mark.parametrize("bits", BITS_MOD + BITS_ODD)
 def test_modexp(mpb, bits, redc):
     count = MODEXP_COUNTS[bits]
     N, base, exp = I.modexp_inputs(config=3, count=count, bits=bits)
@@ -243,8 +246,8 @@ def test_abi_errors_and_noop(mpb):
     with pytest.raises(ValueError):
         mpb.mont_batch_mul(da, da, dN, Np, bits, redc=5)
     with pytest.raises(ValueError):
-        mpb.mp_batch_mul(da, da, 700)  # L = 24 not compiled
-    assert not mpb.supported(700) and mpb.supported(2048) and mpb.supported(4108)
+        mpb.mp_batch_mul(da, da, 20000)  # beyond the 16384-bit maximum
+    assert not mpb.supported(20000) and mpb.supported(700) and mpb.supported(2048) and mpb.supported(4108)
     # count == 0 is a no-op
     z = mpb.empty_sliced(32, 0)
     assert mpb.mp_batch_mul(z, z, bits).shape == (16, 0, 4)

@@ -1,0 +1,180 @@
+"""Measure every BASELINE.json config on one B200 (bench.py times config 3 only).
+
+Prints one JSON object per measurement; each carries the algorithmic IMAD count, the
+roofline fraction (148 SMs x 64 IMAD/clk x 1965 MHz = 18.61 T IMAD/s) and, where cheap,
+a parity verdict against the oracle on a seeded sample.
+
+  python tools/bench_suite.py [--configs 1,2,3,4,5] [--reps 3]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import oracle as O  # noqa: E402  (parity samples only)
+from bench import imad_counts, modexp_imad  # noqa: E402
+from paper_2410_18129_b200 import inputs as I  # noqa: E402
+from paper_2410_18129_b200 import mpb  # noqa: E402
+
+PEAK = 148 * 64 * 1.965e9
+
+
+def timeit(fn, reps: int, warmup: int = 2) -> float:
+    """Mean CUDA-event time (ms) of fn over reps, after warmup."""
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(reps):
+        fn()
+    e1.record(s)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def emit(d: dict) -> None:
+    print(json.dumps(d), flush=True)
+
+
+def sample_idx(count: int, n: int = 16, seed: int = 0) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    idx = rng.choice(count, size=min(n, count), replace=False)
+    return np.unique(np.concatenate([idx, [0, count - 1]]))
+
+
+def config1(reps):
+    bits, count = 1024, 8
+    N, base, exp = I.modexp_inputs(config=1, count=count, bits=bits)
+    _, a, b = I.montmul_inputs(config=1, count=count, bits=bits)
+    dN, dB, dE, da, db = (mpb.to_device(x) for x in (N, base, exp, a, b))
+    Np, R2 = mpb.mont_batch_setup(dN, bits)
+    ref_exp = O.batch_modexp(base, exp, bits, N)
+    for redc, name in ((1, "truncated"), (0, "full")):
+        ws = mpb.modexp_workspace(count, bits, 5)
+        out = mpb.empty_sliced(32, count)
+        ms = timeit(lambda: mpb.mont_batch_modexp_ct(dN, Np, R2, dB, dE, bits, 5, redc, ws=ws, out=out), reps)
+        ok = bool(np.array_equal(mpb.to_host(out), ref_exp))
+        mws = mpb.mont_workspace(count, bits)
+        mm = mpb.to_host(mpb.mont_batch_mul(da, db, dN, Np, bits, redc, ws=mws))
+        ms2 = mpb.to_host(mpb.mont_batch_sqr(da, dN, Np, bits, redc, ws=mws))
+        ok_m = bool(np.array_equal(mm, O.batch_montmul(a, b, N)) and np.array_equal(ms2, O.batch_montmul(a, a, N)))
+        emit({"config": 1, "op": "modexp", "bits": bits, "count": count, "window": 5, "redc": name,
+              "latency_us": 1000 * ms, "parity_modexp": ok, "parity_montmul_montsqr": ok_m})
+
+
+def config2(reps, sizes=(1024, 2048, 3072, 4096)):
+    count = 1 << 20
+    for bits in sizes:
+        L = I.limbs_for_bits(bits)
+        N, a, b = I.montmul_inputs(config=2, count=count, bits=bits)
+        dN, da, db = (mpb.to_device(x) for x in (N, a, b))
+        Np, _ = mpb.mont_batch_setup(dN, bits)
+        ws = mpb.mont_workspace(count, bits)
+        idx = sample_idx(count)
+        for redc, name in ((1, "truncated"), (0, "full")):
+            res = {}
+            for op in ("mul", "sqr"):
+                if op == "mul":
+                    fn = lambda: mpb.mont_batch_mul(da, db, dN, Np, bits, redc, ws=ws)  # noqa: E731
+                else:
+                    fn = lambda: mpb.mont_batch_sqr(da, dN, Np, bits, redc, ws=ws)  # noqa: E731
+                ms = timeit(fn, reps)
+                out = mpb.to_host(fn())
+                ref = O.batch_montmul(a[idx], (b if op == "mul" else a)[idx], N[idx])
+                imad = imad_counts(L, redc == 1)[op] * count
+                bytes_io = (5 if op == "mul" else 4) * L * 4 * count
+                emit({"config": 2, "op": f"mont_{op}", "bits": bits, "count": count, "redc": name,
+                      "ms": ms, "ops_per_s": count / (ms / 1e3), "imad_frac": imad / (ms / 1e3) / PEAK,
+                      "io_gbs": bytes_io / (ms / 1e3) / 1e9, "parity_sample": bool(np.array_equal(out[idx], ref))})
+                res[op] = ms
+            torch.cuda.synchronize()
+        del dN, da, db, Np, ws
+        torch.cuda.empty_cache()
+
+
+def modexp_run(config, bits, count, reps, redcs=((1, "truncated"), (0, "full")), check=8):
+    N, base, exp = I.modexp_inputs(config=config, count=count, bits=bits)
+    dN, dB, dE = (mpb.to_device(x) for x in (N, base, exp))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    Np, R2 = mpb.mont_batch_setup(dN, bits)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t0
+    ws = mpb.modexp_workspace(count, bits, 5)
+    L = I.limbs_for_bits(bits)
+    outs = {}
+    idx = sample_idx(count, check)
+    for redc, name in redcs:
+        out = mpb.empty_sliced(L, count)
+        ms = timeit(lambda: mpb.mont_batch_modexp_ct(dN, Np, R2, dB, dE, bits, 5, redc, ws=ws, out=out), reps, 1)
+        outs[name] = out
+        h = mpb.to_host(out)
+        ok = bool(np.array_equal(h[idx], O.batch_modexp(base[idx], exp[idx], bits, N[idx])))
+        imad = modexp_imad(bits, 5, redc == 1) * count
+        emit({"config": config, "op": "modexp", "bits": bits, "count": count, "window": 5, "redc": name, "ms": ms,
+              "modexp_per_s": count / (ms / 1e3), "imad_frac": imad / (ms / 1e3) / PEAK,
+              "setup_s": setup_s, "parity_sample": ok, "sample": len(idx)})
+    if len(outs) == 2:
+        emit({"config": config, "bits": bits, "truncated_equals_full_on_whole_batch":
+              bool(torch.equal(outs["truncated"], outs["full"]))})
+    del dN, dB, dE, Np, R2, ws, outs
+    torch.cuda.empty_cache()
+
+
+def products(bits, count, reps):
+    L = I.limbs_for_bits(bits)
+    a, b = I.mul_inputs(config=4, count=count, bits=bits)
+    da, db = mpb.to_device(a), mpb.to_device(b)
+    idx = sample_idx(count, 8)
+    for algo, name in ((mpb.ALGO_SCHOOLBOOK, "schoolbook"), (mpb.ALGO_KARATSUBA, "karatsuba")):
+        for op in ("mul", "sqr"):
+            try:
+                fn = (lambda: mpb.mp_batch_mul(da, db, bits, algo)) if op == "mul" else (lambda: mpb.mp_batch_sqr(da, bits, algo))
+                ms = timeit(fn, reps)
+                out = mpb.to_host(fn())
+            except ValueError as e:
+                emit({"config": 4, "op": f"mp_{op}", "bits": bits, "algo": name, "unavailable": str(e)})
+                continue
+            ok = all(I.from_limbs(out[k]) == O.mul(I.from_limbs(a[k]), I.from_limbs((b if op == "mul" else a)[k]))
+                     for k in idx)
+            imad = (2 * L * L if op == "mul" else L * L + L) * count
+            emit({"config": 4, "op": f"mp_{op}", "bits": bits, "count": count, "algo": name, "ms": ms,
+                  "ops_per_s": count / (ms / 1e3), "imad_frac_schoolbook_basis": imad / (ms / 1e3) / PEAK,
+                  "parity_sample": ok})
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="1,2,3,4,5")
+    ap.add_argument("--reps", type=int, default=3)
+    args = ap.parse_args()
+    cfgs = {int(c) for c in args.configs.split(",")}
+    emit({"device": torch.cuda.get_device_name(), "peak_imad_per_s": PEAK})
+    if 1 in cfgs:
+        config1(args.reps)
+    if 2 in cfgs:
+        config2(args.reps)
+    if 3 in cfgs:
+        modexp_run(3, 2048, 1 << 18, args.reps)
+    if 4 in cfgs:
+        modexp_run(4, 4096, 1 << 16, args.reps)
+        modexp_run(4, 4108, 1 << 16, 1, redcs=((1, "truncated"),))
+        products(4096, 1 << 16, args.reps)
+        products(4154, 1 << 16, args.reps)
+    if 5 in cfgs:
+        modexp_run(5, 2048, 1 << 22, 1, redcs=((1, "truncated"),), check=64)
+
+
+if __name__ == "__main__":
+    main()
