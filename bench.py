@@ -59,6 +59,18 @@ def modexp_imad(bits: int, w: int, trunc: bool) -> int:
     return (W - 1) * w * c["sqr"] + ((W - 1) + (1 << w) - 1) * c["mul"] + 2 * c["redc"]
 
 
+def ncu_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per k_modexp launch (TB), from the committed
+    `ncu --set full` capture of this exact launch (profiles/r01_ncu_modexp.json), else None."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_modexp.json")))
+        if d.get("operands_per_launch") == COUNT:
+            return d["dram_bytes_per_launch"] / 1e12
+    except Exception:
+        pass
+    return None
+
+
 # -------------------------------------------------------------------- clocks
 class ClockSampler:
     """Samples SM clock and throttle reasons with NVML during the timed region."""
@@ -255,7 +267,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             "roofline": {
                 "bound": "alu", "kernel": "k_modexp<16,4,true>",
                 "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TIMAD/s", "frac": achieved / peak,
-                "traffic": None,
+                "traffic_unit": "TB per launch (DRAM, ncu; algorithmic table-scan bytes 0.88 TB)",
+                "traffic": ncu_traffic(),
                 "peak_basis": f"{SMS} SMs x {IMAD_PER_CLK_SM} IMAD/clk/SM (K0 measured 63.6) x {f_max/1e6:.0f} MHz",
                 "frac_at_sampled_clock": (achieved / (SMS * IMAD_PER_CLK_SM * clk["sm_mhz"] * 1e6)
                                           if clk["sm_mhz"] else None),
