@@ -251,3 +251,17 @@ def test_abi_errors_and_noop(mpb):
     # count == 0 is a no-op
     z = mpb.empty_sliced(32, 0)
     assert mpb.mp_batch_mul(z, z, bits).shape == (16, 0, 4)
+
+
+def test_sharded_slices_match_whole_batch(mpb):
+    """G logical shards on one device (one stream each) reproduce the whole-batch result
+    byte for byte (SURVEY 8(c) multi-GPU row; the real 1/2/4/8-GPU runs slice the same way)."""
+    from paper_2410_18129_b200 import shard
+
+    bits, count = 1024, 1000
+    N, base, exp = I.modexp_inputs(config=5, count=count, bits=bits)
+    whole = shard.modexp_devices(N, base, exp, bits, devices=[0])
+    for G in (2, 3, 8):
+        assert np.array_equal(shard.modexp_devices(N, base, exp, bits, devices=[0] * G), whole)
+    idx = [0, 1, 499, 998, 999]
+    assert np.array_equal(whole[idx], O.batch_modexp(base[idx], exp[idx], bits, N[idx]))
