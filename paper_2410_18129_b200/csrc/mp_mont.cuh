@@ -359,8 +359,13 @@ MPB_DEVI void ct_select(const Arr& G, int L, int nent, uint32_t idx, const Arr& 
             for (int u = 0; u < U; u++)
 #pragma unroll
                 for (int q = 0; q < GRP; q++)
+#ifdef MPB_PLANTED_BRANCH  // NEGATIVE CONTROL ONLY (tools/ct_check.py): secret-dependent branch + address
+                    v[u][q] = ((uint32_t)(e0 + u) == idx && g0 + q < Q4) ? G.ld_stream((e0 + u) * Q4 + g0 + q)
+                                                                         : make_uint4(0, 0, 0, 0);
+#else
                     v[u][q] = (e0 + u < nent && g0 + q < Q4) ? G.ld_stream((e0 + u) * Q4 + g0 + q)
                                                               : make_uint4(0, 0, 0, 0);
+#endif
 #pragma unroll
             for (int u = 0; u < U; u++) {
                 const uint32_t x = (uint32_t)(e0 + u) ^ idx;
