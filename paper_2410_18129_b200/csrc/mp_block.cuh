@@ -268,29 +268,49 @@ MPB_DEVI void acc_mul(uint32_t (&W)[2 * C + 1], const uint32_t (&x)[C], const ui
     w_add<0, 2 * C, 0>(W, E);
     w_add<1, 2 * C - 1, 0>(W, O);
 }
+// E[1..2C) += O[0..2C-1)  (fold the odd-aligned array into the even one: one carry chain)
+template <int C>
+MPB_DEVI void fold_odd(uint32_t (&E)[2 * C], const uint32_t (&O)[2 * C]) {
+    add_first(E[1], O[0]);
+#pragma unroll
+    for (int k = 2; k < 2 * C - 1; k++) add_next(E[k], O[k - 1]);
+    add_end(E[2 * C - 1], O[2 * C - 2]);
+}
+// W[0..2C] += 2*S for a 2C-word S (shift by one bit with funnel shifts: no carry chain)
+template <int C>
+MPB_DEVI void w_add_double(uint32_t (&W)[2 * C + 1], const uint32_t (&S)[2 * C]) {
+    uint32_t D[2 * C];
+    D[0] = S[0] << 1;
+#pragma unroll
+    for (int k = 1; k < 2 * C; k++) D[k] = __funnelshift_l(S[k - 1], S[k], 1);
+    const uint32_t top = S[2 * C - 1] >> 31;
+    add_first(W[0], D[0]);
+#pragma unroll
+    for (int k = 1; k < 2 * C; k++) add_next(W[k], D[k]);
+    add_end(W[2 * C], top);
+}
 // W[0..2C] += 2*x*y
 template <int C>
 MPB_DEVI void acc_mul2(uint32_t (&W)[2 * C + 1], const uint32_t (&x)[C], const uint32_t (&y)[C]) {
     uint32_t E[2 * C], O[2 * C];
     bp_mul<C>(x, y, E, O);
-    w_add<0, 2 * C, 0>(W, E);
-    w_add<0, 2 * C, 0>(W, E);
-    w_add<1, 2 * C - 1, 0>(W, O);
-    w_add<1, 2 * C - 1, 0>(W, O);
+    fold_odd<C>(E, O);  // E = x*y exactly (< 2^{64C})
+    w_add_double<C>(W, E);
 }
-// W[0..2C] += x^2
+// W[0..2C] += x^2 = D + 2*S with D the diagonal squares (added first: its products and chain do
+// not depend on the off-diagonal rows, so ptxas can overlap them) and S the off-diagonal sum.
 template <int C>
 MPB_DEVI void acc_sqr(uint32_t (&W)[2 * C + 1], const uint32_t (&x)[C]) {
+    {
+        uint32_t D[2 * C];
+#pragma unroll
+        for (int i = 0; i < C; i++) pr_set(D[2 * i], D[2 * i + 1], x[i], x[i]);
+        w_add<0, 2 * C, 0>(W, D);
+    }
     uint32_t E[2 * C], O[2 * C];
     bp_sqr_offdiag<C>(x, E, O);
-    w_add<1, 2 * C - 1, 1>(W, E);  // E[0] == 0; carries run up to W[2C]
-    w_add<1, 2 * C - 1, 1>(W, E);
-    w_add<1, 2 * C - 1, 0>(W, O);  // O[2C-2] == 0 (top off-diagonal position is 2C-2)
-    w_add<1, 2 * C - 1, 0>(W, O);
-    uint32_t D[2 * C];
-#pragma unroll
-    for (int i = 0; i < C; i++) pr_set(D[2 * i], D[2 * i + 1], x[i], x[i]);
-    w_add<0, 2 * C, 0>(W, D);
+    fold_odd<C>(E, O);  // S = sum_{i<j} x_i x_j 2^{32(i+j)} < 2^{64C-1}
+    w_add_double<C>(W, E);
 }
 // W[0..C) += x*y mod 2^{32C}
 template <int C>

@@ -1,5 +1,11 @@
 // Ceiling of the block-product structure: back-to-back acc_mul<C> / acc_sqr<C> on register
 // operands (no memory traffic), at a given number of resident 128-thread CTAs per SM.
+//   MODE 0: acc_mul, operands depend on the previous window (serialised iterations)
+//   MODE 1: acc_sqr, same dependence
+//   MODE 3: acc_mul, independent operands (the real engine: operands come from memory)
+//   MODE 4: acc_mul, independent operands, two block products per iteration (merge of the
+//           first can overlap the products of the second inside one basic block)
+//   MODE 5: acc_sqr, independent operands
 #include <cstdio>
 #include <cuda_runtime.h>
 #include "../paper_2410_18129_b200/csrc/mp_block.cuh"
@@ -17,12 +23,16 @@ __global__ void __launch_bounds__(128) k_blk(uint32_t* out, uint32_t seed, int i
     for (int it = 0; it < iters; it++) {
         if (MODE == 0) acc_mul<C>(W, x, y);
         else if (MODE == 1) acc_sqr<C>(W, x);
-        else { uint32_t E[2 * C], O[2 * C]; bp_mul<C>(x, y, E, O);
-#pragma unroll
-               for (int i = 0; i < 2 * C; i++) W[i & 7] ^= E[i] ^ O[i]; }
-        x[it & (C - 1)] ^= W[C];  // loop-carried dependence keeps the work live
+        else if (MODE == 3) acc_mul<C>(W, x, y);
+        else if (MODE == 4) { acc_mul<C>(W, x, y); acc_mul<C>(W, y, x); }
+        else if (MODE == 5) acc_sqr<C>(W, x);
+        else if (MODE == 6) acc_mul2<C>(W, x, y);
+        if (MODE <= 1) x[it & (C - 1)] ^= W[C];
+        else { x[it & (C - 1)] += 0x9E3779B9u; y[(it + 3) & (C - 1)] ^= 0x85EBCA6Bu; }
 #pragma unroll
         for (int i = 0; i <= C; i++) W[i] = W[i + C];
+#pragma unroll
+        for (int i = C + 1; i <= 2 * C; i++) W[i] = 0;
     }
     __syncthreads();
     long long t1 = clock64();
@@ -42,15 +52,16 @@ void run(const char* name, int blocks_per_sm, double prods_per_iter) {
     unsigned long long cyc[4096]; cudaMemcpyFromSymbol(cyc, g_cyc, sizeof(unsigned long long) * sms * blocks_per_sm);
     unsigned long long mx = 0; for (int i = 0; i < sms * blocks_per_sm; i++) mx = cyc[i] > mx ? cyc[i] : mx;
     double per_clk = prods_per_iter * iters * 128.0 * blocks_per_sm / (double)mx;
-    printf("%-28s C=%2d ctas/SM=%d  products/clk/SM=%.2f  (%.1f%% of 32)\n", name, C, blocks_per_sm, per_clk, per_clk / 32 * 100);
+    printf("%-40s C=%2d ctas/SM=%d  products/clk/SM=%.2f  (%.1f%% of 32)\n", name, C, blocks_per_sm, per_clk, per_clk / 32 * 100);
     cudaFree(d);
 }
 int main() {
-    for (int b : {1, 2, 3, 4}) {
-        run<16, 0>("acc_mul (products+merge)", b, 256);
-        run<16, 2>("bp_mul only", b, 256);
-        run<16, 1>("acc_sqr", b, 136);
+    for (int b : {2, 3}) {
+        run<16, 0>("acc_mul dependent", b, 256);
+        run<16, 3>("acc_mul independent", b, 256);
+        run<16, 6>("acc_mul2 independent", b, 256);
+        run<16, 1>("acc_sqr dependent", b, 136);
+        run<16, 5>("acc_sqr independent", b, 136);
     }
-    for (int b : {3, 5, 6}) { run<8, 0>("acc_mul (products+merge)", b, 64); run<8, 1>("acc_sqr", b, 36); }
     return 0;
 }
