@@ -200,10 +200,6 @@ MPB_DEVI void engine(int ph, int NB, const Arr& AX, const Arr& AY, const Arr& DS
         return false;
     };
     auto issue = [&](int k, int s, int buf) {
-#ifdef MPB_ABLATE_PREFETCH  // timing experiment only: operands are NOT loaded (wrong results)
-        cp_commit();
-        return;
-#endif
         const uint32_t b = sg.base + (uint32_t)(buf * 2 * (C / 4)) * sg.cs;
 #pragma unroll
         for (int q = 0; q < C / 4; q++) cp_async16(b + q * sg.cs, AX.addr(s * (C / 4) + q));
@@ -346,9 +342,7 @@ MPB_DEVI void mont_op(int mode, int NB, const Arr& X, const Arr& B, const Arr& N
 template <int U>
 MPB_DEVI void ct_select(const Arr& G, int L, int nent, uint32_t idx, const Arr& OUT) {
     const int Q4 = L / 4;
-#ifdef MPB_ABLATE_SELECT  // timing experiment only: no table scan (wrong results)
-    return;
-#endif
+
 #ifdef MPB_SEL_G
     constexpr int GRP = MPB_SEL_G;
 #else
