@@ -52,71 +52,6 @@ __global__ void k_contract(const uint4* __restrict__ src, uint4* __restrict__ ds
     dst[k * chunks + q] = src[q * count + k];
 }
 
-// ---------------------------------------------------------------- setup
-// Nprime = (-N)^-1 mod R by word-wise Hensel lifting; R2 = 2^(64L) mod N by doubling.
-// Untimed support kernel (the paper's "precomputed values").  Scratch: A (L+1 words
-// rounded to L+4), X (L) per operand, 32-bit access into the word-sliced layout.
-MPB_DEVI uint32_t* wptr(uint32_t* base, size_t count, size_t k, int i) {
-    return base + ((size_t)(i >> 2) * count + k) * 4 + (i & 3);
-}
-__global__ void k_setup(const uint32_t* __restrict__ N, uint32_t* __restrict__ NP, uint32_t* __restrict__ R2,
-                        size_t count, int L, uint32_t* ws) {
-    const size_t k = tid_global();
-    if (k >= count) return;
-    uint32_t* A = ws;                                  // L + 4 words per operand
-    uint32_t* X = ws + (size_t)(L + 4) * count;       // L words per operand
-    auto n = [&](int i) { return word_at(N, count, k, i); };
-    // n0' = -N0^-1 mod 2^32 (Newton: 5 steps double the correct bits 1 -> 32... start with 3 bits)
-    const uint32_t n0 = n(0);
-    uint32_t inv = n0;  // correct to 3 bits for odd n0
-#pragma unroll
-    for (int it = 0; it < 5; it++) inv *= 2u - n0 * inv;
-    const uint32_t n0p = 0u - inv;
-    // A = 1; for i: x_i = A[i]*n0'; A += x_i * N * 2^(32 i)  (mod R)
-    for (int i = 0; i < L; i++) *wptr(A, count, k, i) = (i == 0);
-    for (int i = 0; i < L; i++) {
-        const uint32_t xi = *wptr(A, count, k, i) * n0p;
-        *wptr(NP, count, k, i) = xi;
-        uint64_t carry = 0;
-        for (int j = 0; i + j < L; j++) {
-            uint32_t* ap = wptr(A, count, k, i + j);
-            const uint64_t t = (uint64_t)xi * n(j) + *ap + carry;
-            *ap = (uint32_t)t;
-            carry = t >> 32;
-        }
-    }
-    // R2: x = 2^(nbits-1) (< N), then 64L - nbits + 1 modular doublings
-    int top = L - 1;
-    while (top > 0 && n(top) == 0) top--;
-    const int nbits = 32 * top + (32 - __clz(n(top)));
-    for (int i = 0; i < L; i++) *wptr(X, count, k, i) = 0;
-    *wptr(X, count, k, (nbits - 1) >> 5) = 1u << ((nbits - 1) & 31);
-    const int steps = 64 * L - nbits + 1;
-    for (int s = 0; s < steps; s++) {
-        // x = 2x (with top bit out), then d = x - N; keep d if (out || no borrow)
-        uint32_t out = 0;
-        for (int i = 0; i < L; i++) {
-            uint32_t* xp = wptr(X, count, k, i);
-            const uint32_t v = *xp;
-            *xp = (v << 1) | out;
-            out = v >> 31;
-        }
-        uint32_t borrow = 0;
-        for (int i = 0; i < L; i++) {
-            const uint32_t v = *wptr(X, count, k, i), m = n(i);
-            const uint64_t d = (uint64_t)v - m - borrow;
-            *wptr(A, count, k, i) = (uint32_t)d;
-            borrow = (uint32_t)(d >> 63);
-        }
-        const uint32_t msk = 0u - ((out | (borrow ^ 1u)) & 1u);
-        for (int i = 0; i < L; i++) {
-            uint32_t* xp = wptr(X, count, k, i);
-            *xp = (*wptr(A, count, k, i) & msk) | (*xp & ~msk);
-        }
-    }
-    for (int i = 0; i < L; i++) *wptr(R2, count, k, i) = *wptr(X, count, k, i);
-}
-
 // ------------------------------------------------------------- dispatch
 // Kernels are instantiated per block size C in {16, 12, 8, 4}; nb = L / C is a runtime
 // argument.  Block size for a limb count: the largest C dividing L (mpb::block_for), unless
@@ -336,7 +271,7 @@ int mont_batch_modexp_ct(const uint32_t* N, const uint32_t* NP, const uint32_t* 
 
 size_t mont_batch_setup_workspace(size_t count, int bits) {
     const int L = mpb_limbs(bits);
-    return count * (size_t)(2 * L + 4) * sizeof(uint32_t);
+    return count * (size_t)(6 * L) * sizeof(uint32_t);
 }
 
 int mont_batch_setup(const uint32_t* N, uint32_t* NP, uint32_t* R2, size_t count, int bits, void* ws, size_t ws_bytes,
@@ -348,8 +283,11 @@ int mont_batch_setup(const uint32_t* N, uint32_t* NP, uint32_t* R2, size_t count
     if (int rc = check_ptrs({N, NP, R2, ws})) return rc;
     if (NP == N || R2 == N || NP == R2) return fail(MPB_EINVAL, "output aliases an input");
     if (ws_bytes < mont_batch_setup_workspace(count, bits)) return fail(MPB_EINVAL, "workspace too small");
-    k_setup<<<grid_for(count), kThreads, 0, (cudaStream_t)stream>>>(N, NP, R2, count, L, (uint32_t*)ws);
-    return check_launch();
+    return dispatch_L(L, [&](auto Ci, int nb) {
+        constexpr int C = decltype(Ci)::value;
+        Launch<C>::setup(N, NP, R2, count, nb, (uint32_t*)ws, (cudaStream_t)stream);
+        return check_launch();
+    });
 }
 
 int mpb_modexp_host(const uint32_t* N, const uint32_t* base, const uint32_t* exp, uint32_t* out, size_t count,

@@ -11,6 +11,7 @@
 #include "launch.h"
 #include "mp_kara.cuh"
 #include "mp_mont.cuh"
+#include "mp_setup.cuh"
 
 namespace mpb {
 
@@ -176,7 +177,29 @@ __global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_modexp(
     }
 }
 
+// ------------------------------------------------------------------- setup
+// N' = (-N)^-1 mod R and R^2 mod N (mp_setup.cuh); workspace 6L words per operand.
+template <int C>
+__global__ void __launch_bounds__(kThreads) k_setup(const uint32_t* __restrict__ N, uint32_t* __restrict__ NP,
+                                                    uint32_t* __restrict__ R2, size_t count, int nb, uint32_t* ws) {
+    const size_t k = tid_global();
+    if (k >= count) return;
+    const int L = C * nb;
+    int top = L - 1;  // bit length of the (public) modulus
+    while (top > 0 && word_at(N, count, k, top) == 0) top--;
+    const int nbits = 32 * top + (32 - __clz(word_at(N, count, k, top)));
+    setup_one<C>(nb, arr(N, count, k), arr(NP, count, k), arr(R2, count, k), arr(ws, count, k), stage(),
+                 word_at(N, count, k, 0), nbits);
+}
+
 // ---------------------------------------------------------------- launchers
+template <int C>
+void Launch<C>::setup(const uint32_t* N, uint32_t* NP, uint32_t* R2, size_t count, int nb, uint32_t* ws,
+                      cudaStream_t s) {
+    k_setup<C><<<(unsigned)((count + kThreads - 1) / kThreads), kThreads, stage_bytes<C>(), s>>>(N, NP, R2, count, nb,
+                                                                                               ws);
+}
+
 inline unsigned grid_for(size_t n) { return (unsigned)((n + kThreads - 1) / kThreads); }
 
 template <int C>

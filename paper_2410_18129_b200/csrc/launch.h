@@ -18,6 +18,9 @@ struct Launch {
                          size_t count, int nb, bool trunc, bool sqr, uint32_t* ws, cudaStream_t s);
     static void mont_redc(const uint32_t* T, const uint32_t* N, const uint32_t* NP, uint32_t* c, size_t count, int nb,
                           bool trunc, uint32_t* ws, cudaStream_t s);
+    // N' = (-N)^-1 mod R and R^2 mod N; ws: 6L words per operand
+    static void setup(const uint32_t* N, uint32_t* NP, uint32_t* R2, size_t count, int nb, uint32_t* ws,
+                      cudaStream_t s);
     static void modexp(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
                        const uint32_t* exp, uint32_t* out, size_t count, int nb, int bits, int window, bool trunc,
                        uint32_t* ws, cudaStream_t s);

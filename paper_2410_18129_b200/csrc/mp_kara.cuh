@@ -141,3 +141,17 @@ MPB_DEVI void kmul(bool sqr, int nb, const Arr& A, const Arr& B, const Arr& OUT,
 }
 
 }  // namespace mpb
+
+namespace mpb {
+
+// One shared, non-inlined engine entry (setup and other support kernels).
+template <int C, bool TRUNC>
+__device__ __noinline__ void engine_call(int ph, int nb, Arr AX, Arr AY, Arr DST, Arr T, Arr N, Arr OUT, uint32_t* ol,
+                                         Stage sg) {
+    uint32_t orlo = ol[0], tl1 = ol[1];
+    engine<C, TRUNC>(ph, nb, AX, AY, DST, T, N, OUT, orlo, tl1, sg);
+    ol[0] = orlo;
+    ol[1] = tl1;
+}
+
+}  // namespace mpb

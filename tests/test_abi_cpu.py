@@ -53,6 +53,9 @@ def test_host_only_helpers(lib):
     lib.mont_batch_modexp_ct_workspace.argtypes = [ctypes.c_size_t, ctypes.c_int, ctypes.c_int, ctypes.c_int]
     assert lib.mont_batch_modexp_ct_workspace(10, 2048, 5, 0) == 10 * 64 * (32 + 5) * 4
     assert lib.mont_batch_modexp_ct_workspace(10, 2048, 7, 0) == 0
+    lib.mont_batch_setup_workspace.restype = ctypes.c_size_t
+    lib.mont_batch_setup_workspace.argtypes = [ctypes.c_size_t, ctypes.c_int]
+    assert lib.mont_batch_setup_workspace(10, 2048) == 10 * 6 * 64 * 4
     lib.mp_batch_workspace.restype = ctypes.c_size_t
     lib.mp_batch_workspace.argtypes = [ctypes.c_size_t, ctypes.c_int, ctypes.c_int]
     assert lib.mp_batch_workspace(10, 4096, 1) == 0  # schoolbook needs none
