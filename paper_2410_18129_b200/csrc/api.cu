@@ -240,10 +240,12 @@ int mont_batch_redc(const uint32_t* T, const uint32_t* N, const uint32_t* NP, ui
     });
 }
 
-size_t mont_batch_modexp_ct_workspace(size_t count, int bits, int window, int /*algo*/) {
+size_t mont_batch_modexp_ct_workspace(size_t count, int bits, int window, int algo) {
     const int L = mpb_limbs(bits);
-    if (window < 1 || window > 6) return 0;
-    return count * (size_t)L * (size_t)((1 << window) + 5) * sizeof(uint32_t);
+    if (L <= 0 || window < 1 || window > 6) return 0;
+    const int C = block_of(L);
+    const size_t kara = (size_t)mpb::kara_scratch_blocks_host(L / C, kara_levels(algo, L)) * C;
+    return count * ((size_t)L * (size_t)((1 << window) + 5) + kara) * sizeof(uint32_t);
 }
 
 int mont_batch_modexp_ct(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
@@ -264,6 +266,7 @@ int mont_batch_modexp_ct(const uint32_t* N, const uint32_t* NP, const uint32_t* 
     return dispatch_L(L, [&](auto Ci, int nb) {
         constexpr int C = decltype(Ci)::value;
         Launch<C>::modexp(N, NP, R2, base, exp, out, count, nb, bits, window, redc == MPB_REDC_TRUNCATED,
+                          kara_levels(algo, L),
                               (uint32_t*)ws, (cudaStream_t)stream);
         return check_launch();
     });

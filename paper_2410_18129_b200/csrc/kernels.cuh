@@ -104,7 +104,8 @@ __global__ void __launch_bounds__(kThreads) k_mont_redc(const uint32_t* __restri
 //                                  (P:L765-766),  Y = MontMul(Y, S)
 //   last op          out = REDC(Y)
 // workspace per operand (word-sliced, stride count): G (2^w * L) | Y (L) | T (2L) | Q (L) | S (L)
-template <int C, bool TRUNC, int NBT>
+//   | Karatsuba scratch (kara_scratch_blocks(nb, KLEV) blocks; KLEV = algo levels for the products)
+template <int C, bool TRUNC, int NBT, int KLEV>
 __global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_modexp(
     const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP, const uint32_t* __restrict__ R2,
     const uint32_t* __restrict__ base, const uint32_t* __restrict__ exp, uint32_t* __restrict__ out, size_t count,
@@ -124,6 +125,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_modexp(
     const Arr Q = arr(p, count, k);
     p += (size_t)L * count;
     const Arr S = arr(p, count, k);
+    p += (size_t)L * count;
+    const Arr KS = arr(p, count, k);  // Karatsuba scratch (KLEV > 0)
     const Arr Nn = arr(N, count, k), NPn = arr(NP, count, k), R2n = arr(R2, count, k), Bn = arr(base, count, k);
     const Arr On = arr(out, count, k);
     const Stage sg = stage();
@@ -173,7 +176,7 @@ __global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_modexp(
                 T.st(Q4 + q, make_uint4(0, 0, 0, 0));
             }
         }
-        mont_op<C, TRUNC>(mode, nb, X, B, Nn, NPn, T, Q, O, sg);
+        mont_op_k<C, TRUNC, KLEV>(mode, nb, X, B, Nn, NPn, T, Q, O, KS, sg);
     }
 }
 
@@ -266,17 +269,26 @@ void Launch<C>::mont_redc(const uint32_t* T, const uint32_t* N, const uint32_t* 
 template <int C>
 void Launch<C>::modexp(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
                        const uint32_t* exp, uint32_t* out, size_t count, int nb, int bits, int window, bool trunc,
-                       uint32_t* ws, cudaStream_t s) {
+                       int levels, uint32_t* ws, cudaStream_t s) {
     const size_t sm = stage_bytes<C>();
+    const unsigned g = grid_for(count);
     with_nb<C>(nb, [&](auto NBc) {
         constexpr int NBT = decltype(NBc)::value;
-        if (trunc) {
-            k_modexp<C, true, NBT><<<grid_for(count), kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, nb, bits,
-                                                                        window, ws);
-        } else {
-            k_modexp<C, false, NBT><<<grid_for(count), kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, nb, bits,
-                                                                         window, ws);
+        auto go = [&](auto KL) {
+            constexpr int KLEV = decltype(KL)::value;
+            if (trunc)
+                k_modexp<C, true, NBT, KLEV><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, nb, bits, window,
+                                                                    ws);
+            else
+                k_modexp<C, false, NBT, KLEV><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, nb, bits,
+                                                                     window, ws);
+        };
+        // Karatsuba product phases are compiled for the large shapes only (f1); elsewhere schoolbook
+        if constexpr (NBT == 0 || NBT == 8 || NBT == 11) {
+            if (levels >= 2) return go(std::integral_constant<int, 2>{});
+            if (levels == 1) return go(std::integral_constant<int, 1>{});
         }
+        go(std::integral_constant<int, 0>{});
     });
 }
 

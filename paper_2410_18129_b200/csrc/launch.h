@@ -21,9 +21,10 @@ struct Launch {
     // N' = (-N)^-1 mod R and R^2 mod N; ws: 6L words per operand
     static void setup(const uint32_t* N, uint32_t* NP, uint32_t* R2, size_t count, int nb, uint32_t* ws,
                       cudaStream_t s);
+    // levels: Karatsuba levels of the product phases (0 = schoolbook)
     static void modexp(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
                        const uint32_t* exp, uint32_t* out, size_t count, int nb, int bits, int window, bool trunc,
-                       uint32_t* ws, cudaStream_t s);
+                       int levels, uint32_t* ws, cudaStream_t s);
 };
 
 #define MPB_BLOCKS(X) X(16) X(12) X(8) X(4)

@@ -155,3 +155,21 @@ __device__ __noinline__ void engine_call(int ph, int nb, Arr AX, Arr AY, Arr DST
 }
 
 }  // namespace mpb
+
+namespace mpb {
+
+// Montgomery operation whose product phase (T = X*B or X^2) uses KLEV levels of block Karatsuba
+// (Karatsuba inside MontMul/MontSqr); the reduction phases stay on the engine.
+// KS: kara_scratch_blocks(NB, KLEV) blocks of scratch.  KLEV = 0 is mont_op.
+template <int C, bool TRUNC, int KLEV>
+MPB_DEVI void mont_op_k(int mode, int NB, const Arr& X, const Arr& B, const Arr& N, const Arr& NP, const Arr& T,
+                        const Arr& Q, const Arr& OUT, const Arr& KS, const Stage& sg) {
+    if constexpr (KLEV == 0) {
+        mont_op<C, TRUNC>(mode, NB, X, B, N, NP, T, Q, OUT, sg);
+    } else {
+        if (mode != MODE_REDC) kmul<C, KLEV>(mode == MODE_SQR, NB, X, B, T, KS, sg);
+        mont_op<C, TRUNC>(MODE_REDC, NB, X, B, N, NP, T, Q, OUT, sg);
+    }
+}
+
+}  // namespace mpb

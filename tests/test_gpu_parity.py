@@ -265,3 +265,16 @@ def test_sharded_slices_match_whole_batch(mpb):
         assert np.array_equal(shard.modexp_devices(N, base, exp, bits, devices=[0] * G), whole)
     idx = [0, 1, 499, 998, 999]
     assert np.array_equal(whole[idx], O.batch_modexp(base[idx], exp[idx], bits, N[idx]))
+
+
+@pytest.mark.parametrize("algo", [2, 3])
+@pytest.mark.parametrize("bits", [1536, 3072, 4096, 4108])
+def test_modexp_karatsuba_products(mpb, bits, algo):
+    """Karatsuba (1 and 2 levels) in the product phase of every MontMul/MontSqr."""
+    count = 5
+    N, base, exp = I.modexp_inputs(config=4, count=count, bits=bits)
+    dN = mpb.to_device(N)
+    Np, R2 = mpb.mont_batch_setup(dN, bits)
+    out = mpb.to_host(mpb.mont_batch_modexp_ct(dN, Np, R2, mpb.to_device(base), mpb.to_device(exp), bits,
+                                               window=5, algo=algo))
+    assert np.array_equal(out, O.batch_modexp(base, exp, bits, N))

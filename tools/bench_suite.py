@@ -103,7 +103,7 @@ def config2(reps, sizes=(1024, 2048, 3072, 4096)):
         torch.cuda.empty_cache()
 
 
-def modexp_run(config, bits, count, reps, redcs=((1, "truncated"), (0, "full")), check=8):
+def modexp_run(config, bits, count, reps, redcs=((1, "truncated"), (0, "full")), check=8, algo=0):
     N, base, exp = I.modexp_inputs(config=config, count=count, bits=bits)
     dN, dB, dE = (mpb.to_device(x) for x in (N, base, exp))
     torch.cuda.synchronize()
@@ -111,18 +111,20 @@ def modexp_run(config, bits, count, reps, redcs=((1, "truncated"), (0, "full")),
     Np, R2 = mpb.mont_batch_setup(dN, bits)
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
-    ws = mpb.modexp_workspace(count, bits, 5)
+    ws = mpb.modexp_workspace(count, bits, 5, algo)
     L = I.limbs_for_bits(bits)
     outs = {}
     idx = sample_idx(count, check)
     for redc, name in redcs:
         out = mpb.empty_sliced(L, count)
-        ms = timeit(lambda: mpb.mont_batch_modexp_ct(dN, Np, R2, dB, dE, bits, 5, redc, ws=ws, out=out), reps, 1)
+        ms = timeit(lambda: mpb.mont_batch_modexp_ct(dN, Np, R2, dB, dE, bits, 5, redc, algo=algo, ws=ws, out=out),
+                    reps, 1)
         outs[name] = out
         h = mpb.to_host(out)
         ok = bool(np.array_equal(h[idx], O.batch_modexp(base[idx], exp[idx], bits, N[idx])))
         imad = modexp_imad(bits, 5, redc == 1) * count
-        emit({"config": config, "op": "modexp", "bits": bits, "count": count, "window": 5, "redc": name, "ms": ms,
+        emit({"config": config, "op": "modexp", "bits": bits, "count": count, "window": 5, "redc": name,
+              "algo": ["auto", "schoolbook", "karatsuba", "karatsuba2"][algo], "ms": ms,
               "modexp_per_s": count / (ms / 1e3), "imad_frac": imad / (ms / 1e3) / PEAK,
               "setup_s": setup_s, "parity_sample": ok, "sample": len(idx)})
     if len(outs) == 2:
@@ -170,6 +172,8 @@ def main():
     if 4 in cfgs:
         modexp_run(4, 4096, 1 << 16, args.reps)
         modexp_run(4, 4108, 1 << 16, 1, redcs=((1, "truncated"),))
+        for algo in (2, 3):
+            modexp_run(4, 4096, 1 << 16, args.reps, redcs=((1, "truncated"),), algo=algo)
         products(4096, 1 << 16, args.reps)
         products(4154, 1 << 16, args.reps)
     if 5 in cfgs:
