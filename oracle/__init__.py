@@ -57,6 +57,7 @@ def lib():
             "o_gen_prime": (i, [i, u64, _u32p]),
             "o_montred_classic": (i, [_u32p, _u32p, _u32p, i, _u32p]),
             "o_montred_truncated": (i, [_u32p, _u32p, _u32p, i, _u32p, _u32p]),
+            "o_montmul_cios": (i, [_u32p, _u32p, _u32p, ctypes.c_uint32, i, _u32p]),
             "o_batch_modexp": (i, [_u32p, _u32p, i, _u32p, i, _u32p, sz, i]),
             "o_batch_montmul": (i, [_u32p, _u32p, _u32p, i, _u32p, sz, i]),
         }
@@ -181,6 +182,14 @@ def montred_truncated(T: int, N: int, Nprime: int, L: int) -> tuple[int, int]:
     C, Q = np.zeros(L + 1, np.uint32), np.zeros(L + 1, np.uint32)
     lib().o_montred_truncated(_p(Tt), _p(Nn), _p(NP), L, _p(C), _p(Q))
     return from_limbs(C), from_limbs(Q)
+
+
+def montmul_cios(a: int, b: int, N: int, n0p: int, L: int) -> int:
+    """alg:8BlockMontRed word by word: a*b*R^-1 mod N up to one N (< 2N)."""
+    A, B, Nn, C = _arr(a, L), _arr(b, L), _arr(N, L), np.zeros(L + 1, np.uint32)
+    if lib().o_montmul_cios(_p(A), _p(B), _p(Nn), n0p, L, _p(C)) != 0:
+        raise ValueError("a low word of Y + q*N did not vanish")
+    return from_limbs(C)
 
 
 # ---------------------------------------------------------- batch interface

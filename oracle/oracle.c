@@ -504,6 +504,36 @@ int o_montred_truncated(const uint32_t* T, const uint32_t* N, const uint32_t* Np
     return 0;
 }
 
+/* alg:8BlockMontRed, the CIOS-inspired interleaved Montgomery multiplication,
+ * step by step in 32-bit words (the paper's 52-bit word becomes a 32-bit limb; only
+ * n0' = N' mod 2^32 is used):
+ *   Y <- a[0]*B;  q <- Y mod 2^32 * n0' mod 2^32;  Y <- (Y + q*N) / 2^32     (lines 2-4)
+ *   for i = 1 .. L-1:  Y <- Y + a[i]*B;  q <- ...;  Y <- (Y + q*N) / 2^32      (lines 5-9)
+ * Y has L+2 limbs of room; the result (returned with L+1 limbs) is < 2N for a, b < N. */
+int o_montmul_cios(const uint32_t* a, const uint32_t* B, const uint32_t* N, uint32_t n0p, int L, uint32_t* C) {
+    const size_t W = (size_t)L + 2;
+    uint32_t* Y = zalloc(W);
+    uint32_t* t = zalloc(W);
+    for (int i = 0; i < L; i++) {
+        /* Y <- Y + a[i]*B */
+        memset(t, 0, sizeof(uint32_t) * W);
+        o_mul(&a[i], 1, B, L, t);
+        bn_add(Y, Y, t, (int)W);
+        /* q <- |Y|_{2^32} * n0' mod 2^32 */
+        uint32_t q = Y[0] * n0p;
+        /* Y <- (Y + q*N) / 2^32 : the low word becomes zero, then shift one word down */
+        memset(t, 0, sizeof(uint32_t) * W);
+        o_mul(&q, 1, N, L, t);
+        bn_add(Y, Y, t, (int)W);
+        if (Y[0] != 0) { free(Y); free(t); return -1; }
+        memmove(Y, Y + 1, sizeof(uint32_t) * (W - 1));
+        Y[W - 1] = 0;
+    }
+    memcpy(C, Y, sizeof(uint32_t) * ((size_t)L + 1));
+    free(Y); free(t);
+    return 0;
+}
+
 /* ------------------------------------------------------ batch drivers */
 
 typedef struct {

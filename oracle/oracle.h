@@ -60,6 +60,10 @@ int o_montred_classic(const uint32_t* T, const uint32_t* N, const uint32_t* Npri
 int o_montred_truncated(const uint32_t* T, const uint32_t* N, const uint32_t* Nprime, int L,
                         uint32_t* C, uint32_t* qnhat_out);
 
+/* alg:8BlockMontRed, CIOS in 32-bit words with n0' = N' mod 2^32 only:
+ * C = a*B*R^-1 mod N up to one N (C < 2N), L+1 limbs; -1 if a low word fails to vanish. */
+int o_montmul_cios(const uint32_t* a, const uint32_t* B, const uint32_t* N, uint32_t n0p, int L, uint32_t* C);
+
 /* ---- batch drivers (pthreads over independent items; operand-major arrays) ---- */
 int o_batch_modexp(const uint32_t* base, const uint32_t* e, int ebits, const uint32_t* N, int L,
                    uint32_t* out, size_t count, int threads);

@@ -177,6 +177,24 @@ def test_montmul_definition_and_roundtrip(bits):
         assert O.redc(T, N, L) == c
 
 
+@pytest.mark.parametrize("bits", [32, 64, 1024, 2048, 4096])
+def test_cios_route_matches_definition(bits):
+    """alg:8BlockMontRed step by step with n0' only (A10) lands within one N of the
+    plain definition a*b*R^-1 mod N, including the extreme operands 0, 1 and N-1."""
+    L = I.limbs_for_bits(bits)
+    R = 1 << (32 * L)
+    for _ in range(4):
+        N = RNG.getrandbits(bits) | 1 | (1 << (bits - 1))
+        Np, _ = O.setup(N, L)
+        n0p = Np & 0xFFFFFFFF
+        assert (N * n0p) % (1 << 32) == (1 << 32) - 1  # n0' = -N^-1 mod 2^32
+        for a, b in [(RNG.randrange(N), RNG.randrange(N)), (0, RNG.randrange(N)), (1, 1), (N - 1, N - 1)]:
+            C = O.montmul_cios(a, b, N, n0p, L)
+            assert C < 2 * N
+            assert (C * R - a * b) % N == 0
+            assert (C - N if C >= N else C) == O.montmul(a, b, N, L)
+
+
 # ------------------------------------------- truncated REDC reading (A6 / A7)
 @pytest.mark.parametrize("bits", [64, 128, 1024, 2048])
 def test_truncated_reading_random_and_adversarial(bits):
