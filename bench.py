@@ -41,21 +41,32 @@ SMS, IMAD_PER_CLK_SM = 148, 64  # K0-measured 63.6 (profiles/r01_microbench_int.
 
 
 # ------------------------------------------------------------------ roofline
-def imad_counts(L: int, trunc: bool) -> dict:
+def block_for(L: int) -> int:
+    """Limbs per block of the kernels (the largest of 16, 12, 8, 4 dividing L)."""
+    return next(c for c in (16, 12, 8, 4) if L % c == 0)
+
+
+def imad_counts(L: int, redc: int) -> dict:
     """Algorithmic IMAD per operation: a 32x32->64 word product = 2 IMAD,
-    a lo-only product = 1; the hi-only products of column L-2 count 1 each."""
-    if trunc:
-        mul, sqr, redc = 4 * L * L + 2 * L - 1, 3 * L * L + 3 * L - 1, 2 * L * L + 2 * L - 1
+    a lo-only product = 1; the hi-only products of column L-2 count 1 each.
+    redc: 1 truncated, 0 full, 2 CIOS (alg:8BlockMontRed at digit 2^(32C): per row of C limbs,
+    2CL products for a_i*B, 2CL for m_i*N and a C x C low-half product of C^2 IMAD, so
+    4L^2 + LC for a multiplication or a squaring; REDC is MontMul(X, 1))."""
+    if redc == 2:
+        C = block_for(L)
+        mul = sqr = redc_ = 4 * L * L + L * C
+    elif redc:
+        mul, sqr, redc_ = 4 * L * L + 2 * L - 1, 3 * L * L + 3 * L - 1, 2 * L * L + 2 * L - 1
     else:
-        mul, sqr, redc = 5 * L * L, 4 * L * L + L, 3 * L * L
-    return {"mul": mul, "sqr": sqr, "redc": redc}
+        mul, sqr, redc_ = 5 * L * L, 4 * L * L + L, 3 * L * L
+    return {"mul": mul, "sqr": sqr, "redc": redc_}
 
 
-def modexp_imad(bits: int, w: int, trunc: bool) -> int:
+def modexp_imad(bits: int, w: int, redc: int) -> int:
     """(W-1)*w MontSqr + (W-1) + (2^w - 1) MontMul + 2 REDC."""
     L = I.limbs_for_bits(bits)
     W = -(-bits // w)
-    c = imad_counts(L, trunc)
+    c = imad_counts(L, int(redc))
     return (W - 1) * w * c["sqr"] + ((W - 1) + (1 << w) - 1) * c["mul"] + 2 * c["redc"]
 
 

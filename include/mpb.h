@@ -41,7 +41,12 @@ extern "C" {
 #endif
 
 typedef enum { MPB_OK = 0, MPB_EINVAL = -1, MPB_EUNSUPPORTED = -2, MPB_ECUDA = -3 } mpb_status;
-enum { MPB_REDC_FULL = 0, MPB_REDC_TRUNCATED = 1 };
+/* FULL: alg:8MontRed; TRUNCATED: alg:trunc_montred (Theorems 1-2);
+ * CIOS: alg:8BlockMontRed, reduction interleaved with the rows of a schoolbook
+ * multiplication at the engine's block granularity (digit 2^(32C), uses only the low block of
+ * Nprime).  CIOS applies to mont_batch_mul/sqr and the exponentiation (schoolbook only), not
+ * to a stand-alone mont_batch_redc (MPB_EUNSUPPORTED). */
+enum { MPB_REDC_FULL = 0, MPB_REDC_TRUNCATED = 1, MPB_REDC_CIOS = 2 };
 /* AUTO = the measured crossover; KARATSUBA = one level, KARATSUBA2 = two levels. */
 enum { MPB_ALGO_AUTO = 0, MPB_ALGO_SCHOOLBOOK = 1, MPB_ALGO_KARATSUBA = 2, MPB_ALGO_KARATSUBA2 = 3 };
 
@@ -64,8 +69,8 @@ int mp_batch_sqr(const uint32_t* a, uint32_t* c, size_t count, int bits, int alg
                  size_t workspace_bytes, void* stream);
 size_t mp_batch_workspace(size_t count, int bits, int algo);
 
-/* c = a*b*R^-1 mod N (canonical).  redc = MPB_REDC_TRUNCATED (alg:trunc_montred)
- * or MPB_REDC_FULL (alg:8MontRed).  Nprime is the full (-N)^-1 mod R (limb 0 is
+/* c = a*b*R^-1 mod N (canonical).  redc = MPB_REDC_TRUNCATED (alg:trunc_montred),
+ * MPB_REDC_FULL (alg:8MontRed) or MPB_REDC_CIOS (alg:8BlockMontRed).  Nprime is the full (-N)^-1 mod R (limb 0 is
  * the n0' of CIOS).  workspace: mont_batch_workspace(count, bits) bytes of device memory. */
 int mont_batch_mul(const uint32_t* a, const uint32_t* b, const uint32_t* N, const uint32_t* Nprime,
                    uint32_t* c, size_t count, int bits, int redc, void* workspace, size_t workspace_bytes,

@@ -196,10 +196,12 @@ size_t mont_batch_workspace(size_t count, int bits) {
     return count * (size_t)(3 * L) * sizeof(uint32_t);
 }
 
+static bool redc_ok(int redc) { return redc == MPB_REDC_FULL || redc == MPB_REDC_TRUNCATED || redc == MPB_REDC_CIOS; }
+
 static int mont_op(const uint32_t* a, const uint32_t* b, const uint32_t* N, const uint32_t* NP, uint32_t* c,
                    size_t count, int bits, int redc, void* ws, size_t ws_bytes, bool sqr, void* stream) {
     g_err.clear();
-    if (redc != MPB_REDC_FULL && redc != MPB_REDC_TRUNCATED) return fail(MPB_EINVAL, "redc out of range");
+    if (!redc_ok(redc)) return fail(MPB_EINVAL, "redc out of range");
     int L;
     if (int rc = limbs_checked(bits, L)) return rc;
     if (count == 0) return MPB_OK;
@@ -208,8 +210,7 @@ static int mont_op(const uint32_t* a, const uint32_t* b, const uint32_t* N, cons
     if (ws_bytes < mont_batch_workspace(count, bits)) return fail(MPB_EINVAL, "workspace too small");
     return dispatch_L(L, [&](auto Ci, int nb) {
         constexpr int C = decltype(Ci)::value;
-        Launch<C>::mont_mul(a, b, N, NP, c, count, nb, redc == MPB_REDC_TRUNCATED, sqr, (uint32_t*)ws,
-                                (cudaStream_t)stream);
+        Launch<C>::mont_mul(a, b, N, NP, c, count, nb, redc, sqr, (uint32_t*)ws, (cudaStream_t)stream);
         return check_launch();
     });
 }
@@ -226,7 +227,10 @@ int mont_batch_sqr(const uint32_t* a, const uint32_t* N, const uint32_t* NP, uin
 int mont_batch_redc(const uint32_t* T, const uint32_t* N, const uint32_t* NP, uint32_t* c, size_t count, int bits,
                     int redc, void* ws, size_t ws_bytes, void* stream) {
     g_err.clear();
-    if (redc != MPB_REDC_FULL && redc != MPB_REDC_TRUNCATED) return fail(MPB_EINVAL, "redc out of range");
+    if (!redc_ok(redc)) return fail(MPB_EINVAL, "redc out of range");
+    if (redc == MPB_REDC_CIOS)
+        return fail(MPB_EUNSUPPORTED, "CIOS interleaves the reduction with a multiplication (alg:8BlockMontRed); "
+                                      "a stand-alone REDC takes MPB_REDC_FULL or MPB_REDC_TRUNCATED");
     int L;
     if (int rc = limbs_checked(bits, L)) return rc;
     if (count == 0) return MPB_OK;
@@ -252,9 +256,12 @@ int mont_batch_modexp_ct(const uint32_t* N, const uint32_t* NP, const uint32_t* 
                          const uint32_t* exp, uint32_t* out, size_t count, int bits, int window, int redc, int algo,
                          void* ws, size_t ws_bytes, void* stream) {
     g_err.clear();
-    if (redc != MPB_REDC_FULL && redc != MPB_REDC_TRUNCATED) return fail(MPB_EINVAL, "redc out of range");
+    if (!redc_ok(redc)) return fail(MPB_EINVAL, "redc out of range");
     if (algo < MPB_ALGO_AUTO || algo > MPB_ALGO_KARATSUBA2) return fail(MPB_EINVAL, "algo out of range");
     if (window < 1 || window > 6) return fail(MPB_EINVAL, "window must be in 1..6");
+    if (redc == MPB_REDC_CIOS && (algo == MPB_ALGO_KARATSUBA || algo == MPB_ALGO_KARATSUBA2))
+        return fail(MPB_EUNSUPPORTED, "CIOS (alg:8BlockMontRed) interleaves rows of a schoolbook product; "
+                                      "Karatsuba needs MPB_REDC_FULL or MPB_REDC_TRUNCATED");
     int L;
     if (int rc = limbs_checked(bits, L)) return rc;
     if (count == 0) return MPB_OK;
@@ -265,9 +272,8 @@ int mont_batch_modexp_ct(const uint32_t* N, const uint32_t* NP, const uint32_t* 
         return fail(MPB_EINVAL, "workspace too small");
     return dispatch_L(L, [&](auto Ci, int nb) {
         constexpr int C = decltype(Ci)::value;
-        Launch<C>::modexp(N, NP, R2, base, exp, out, count, nb, bits, window, redc == MPB_REDC_TRUNCATED,
-                          kara_levels(algo, L),
-                              (uint32_t*)ws, (cudaStream_t)stream);
+        Launch<C>::modexp(N, NP, R2, base, exp, out, count, nb, bits, window, redc,
+                          redc == MPB_REDC_CIOS ? 0 : kara_levels(algo, L), (uint32_t*)ws, (cudaStream_t)stream);
         return check_launch();
     });
 }
@@ -298,6 +304,7 @@ int mpb_modexp_host(const uint32_t* N, const uint32_t* base, const uint32_t* exp
     g_err.clear();
     int L;
     if (int rc = limbs_checked(bits, L)) return rc;
+    if (!redc_ok(redc)) return fail(MPB_EINVAL, "redc out of range");
     if (count == 0) return MPB_OK;
     if (!N || !base || !exp || !out) return fail(MPB_EINVAL, "null pointer");
     cudaStream_t s = (cudaStream_t)stream;

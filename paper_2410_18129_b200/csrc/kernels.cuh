@@ -65,8 +65,9 @@ __global__ void __launch_bounds__(kThreads) k_mp_mul(const uint32_t* __restrict_
     }
 }
 
-// workspace for the mont kernels: T (2L) then Q (L), word-sliced with stride count
-template <int C, bool TRUNC, bool SQR, int NBT>
+// workspace for the mont kernels: T (2L) then Q (L), word-sliced with stride count.
+// RM: 0 full, 1 truncated, 2 CIOS (mont_op_rm).
+template <int C, int RM, bool SQR, int NBT>
 __global__ void __launch_bounds__(kThreads) k_mont_mul(const uint32_t* __restrict__ a, const uint32_t* __restrict__ b,
                                                        const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP,
                                                        uint32_t* __restrict__ c, size_t count, int nb_rt, uint32_t* ws) {
@@ -75,8 +76,9 @@ __global__ void __launch_bounds__(kThreads) k_mont_mul(const uint32_t* __restric
     const int nb = NBT ? NBT : nb_rt;
     const size_t L = (size_t)C * nb;
     const Arr T = arr(ws, count, k), Q = arr(ws + 2 * L * count, count, k);
-    mont_op<C, TRUNC>(SQR ? MODE_SQR : MODE_MUL, nb, arr(a, count, k), arr(SQR ? a : b, count, k), arr(N, count, k),
-                      arr(NP, count, k), T, Q, arr(c, count, k), stage());
+    const Arr A = arr(a, count, k);
+    mont_op_rm<C, RM, 0>(SQR ? MODE_SQR : MODE_MUL, nb, A, SQR ? A : arr(b, count, k), arr(N, count, k),
+                         arr(NP, count, k), T, Q, arr(c, count, k), Q, stage());
 }
 
 template <int C, bool TRUNC>
@@ -105,7 +107,7 @@ __global__ void __launch_bounds__(kThreads) k_mont_redc(const uint32_t* __restri
 //   last op          out = REDC(Y)
 // workspace per operand (word-sliced, stride count): G (2^w * L) | Y (L) | T (2L) | Q (L) | S (L)
 //   | Karatsuba scratch (kara_scratch_blocks(nb, KLEV) blocks; KLEV = algo levels for the products)
-template <int C, bool TRUNC, int NBT, int KLEV>
+template <int C, int RM, int NBT, int KLEV>
 __global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_modexp(
     const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP, const uint32_t* __restrict__ R2,
     const uint32_t* __restrict__ base, const uint32_t* __restrict__ exp, uint32_t* __restrict__ out, size_t count,
@@ -169,14 +171,14 @@ __global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_modexp(
             ct_select<select_unroll<C>()>(G, L, nent, v & ((1u << w) - 1u), O);
             continue;
         }
-        if (mode == MODE_REDC) {  // T = X zero-extended to 2L limbs
+        if (RM != 2 && mode == MODE_REDC) {  // T = X zero-extended to 2L limbs (CIOS: MontMul(X, 1))
 #pragma unroll 1
             for (int q = 0; q < Q4; q++) {
                 T.st(q, X.ld(q));
                 T.st(Q4 + q, make_uint4(0, 0, 0, 0));
             }
         }
-        mont_op_k<C, TRUNC, KLEV>(mode, nb, X, B, Nn, NPn, T, Q, O, KS, sg);
+        mont_op_rm<C, RM, KLEV>(mode, nb, X, B, Nn, NPn, T, Q, O, KS, sg);
     }
 }
 
@@ -245,18 +247,19 @@ void with_nb(int nb, F&& f) {
 
 template <int C>
 void Launch<C>::mont_mul(const uint32_t* a, const uint32_t* b, const uint32_t* N, const uint32_t* NP, uint32_t* c,
-                         size_t count, int nb, bool trunc, bool sqr, uint32_t* ws, cudaStream_t s) {
+                         size_t count, int nb, int redc, bool sqr, uint32_t* ws, cudaStream_t s) {
     const unsigned g = grid_for(count);
     const size_t sm = stage_bytes<C>();
     with_nb<C>(nb, [&](auto NBc) {
         constexpr int NBT = decltype(NBc)::value;
-        if (trunc) {
-            if (sqr) k_mont_mul<C, true, true, NBT><<<g, kThreads, sm, s>>>(a, a, N, NP, c, count, nb, ws);
-            else k_mont_mul<C, true, false, NBT><<<g, kThreads, sm, s>>>(a, b, N, NP, c, count, nb, ws);
-        } else {
-            if (sqr) k_mont_mul<C, false, true, NBT><<<g, kThreads, sm, s>>>(a, a, N, NP, c, count, nb, ws);
-            else k_mont_mul<C, false, false, NBT><<<g, kThreads, sm, s>>>(a, b, N, NP, c, count, nb, ws);
-        }
+        auto go = [&](auto RMc) {
+            constexpr int RM = decltype(RMc)::value;
+            if (sqr) k_mont_mul<C, RM, true, NBT><<<g, kThreads, sm, s>>>(a, a, N, NP, c, count, nb, ws);
+            else k_mont_mul<C, RM, false, NBT><<<g, kThreads, sm, s>>>(a, b, N, NP, c, count, nb, ws);
+        };
+        if (redc == 2) go(std::integral_constant<int, 2>{});
+        else if (redc == 1) go(std::integral_constant<int, 1>{});
+        else go(std::integral_constant<int, 0>{});
     });
 }
 template <int C>
@@ -268,20 +271,24 @@ void Launch<C>::mont_redc(const uint32_t* T, const uint32_t* N, const uint32_t* 
 }
 template <int C>
 void Launch<C>::modexp(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
-                       const uint32_t* exp, uint32_t* out, size_t count, int nb, int bits, int window, bool trunc,
+                       const uint32_t* exp, uint32_t* out, size_t count, int nb, int bits, int window, int redc,
                        int levels, uint32_t* ws, cudaStream_t s) {
     const size_t sm = stage_bytes<C>();
     const unsigned g = grid_for(count);
     with_nb<C>(nb, [&](auto NBc) {
         constexpr int NBT = decltype(NBc)::value;
+        if (redc == 2) {  // CIOS: schoolbook rows only
+            k_modexp<C, 2, NBT, 0><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, nb, bits, window, ws);
+            return;
+        }
         auto go = [&](auto KL) {
             constexpr int KLEV = decltype(KL)::value;
-            if (trunc)
-                k_modexp<C, true, NBT, KLEV><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, nb, bits, window,
-                                                                    ws);
+            if (redc == 1)
+                k_modexp<C, 1, NBT, KLEV><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, nb, bits, window,
+                                                                 ws);
             else
-                k_modexp<C, false, NBT, KLEV><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, nb, bits,
-                                                                     window, ws);
+                k_modexp<C, 0, NBT, KLEV><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, nb, bits, window,
+                                                                 ws);
         };
         // Karatsuba product phases are compiled for the large shapes only (f1); elsewhere schoolbook
         if constexpr (NBT == 0 || NBT == 8 || NBT == 11) {

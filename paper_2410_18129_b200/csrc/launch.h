@@ -14,8 +14,9 @@ struct Launch {
     // c = a*b (sqr: a^2), 2L limbs; levels = Karatsuba levels (0 = schoolbook); ws: scratch
     static void mp_mul(const uint32_t* a, const uint32_t* b, uint32_t* c, size_t count, int nb, bool sqr, int levels,
                        uint32_t* ws, cudaStream_t s);
+    // redc: 0 full, 1 truncated, 2 CIOS
     static void mont_mul(const uint32_t* a, const uint32_t* b, const uint32_t* N, const uint32_t* NP, uint32_t* c,
-                         size_t count, int nb, bool trunc, bool sqr, uint32_t* ws, cudaStream_t s);
+                         size_t count, int nb, int redc, bool sqr, uint32_t* ws, cudaStream_t s);
     static void mont_redc(const uint32_t* T, const uint32_t* N, const uint32_t* NP, uint32_t* c, size_t count, int nb,
                           bool trunc, uint32_t* ws, cudaStream_t s);
     // N' = (-N)^-1 mod R and R^2 mod N; ws: 6L words per operand
@@ -23,7 +24,7 @@ struct Launch {
                       cudaStream_t s);
     // levels: Karatsuba levels of the product phases (0 = schoolbook)
     static void modexp(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
-                       const uint32_t* exp, uint32_t* out, size_t count, int nb, int bits, int window, bool trunc,
+                       const uint32_t* exp, uint32_t* out, size_t count, int nb, int bits, int window, int redc,
                        int levels, uint32_t* ws, cudaStream_t s);
 };
 

@@ -172,4 +172,18 @@ MPB_DEVI void mont_op_k(int mode, int NB, const Arr& X, const Arr& B, const Arr&
     }
 }
 
+// Any REDC mode: RM = 0 full (alg:8MontRed), 1 truncated (alg:trunc_montred), 2 CIOS
+// (alg:8BlockMontRed, schoolbook only: the reduction is interleaved with the product rows).
+// CIOS uses T as its Y scratch and Q as its m scratch; REDC(X) is MontMul(X, 1).
+template <int C, int RM, int KLEV>
+MPB_DEVI void mont_op_rm(int mode, int NB, const Arr& X, const Arr& B, const Arr& N, const Arr& NP, const Arr& T,
+                         const Arr& Q, const Arr& OUT, const Arr& KS, const Stage& sg) {
+    if constexpr (RM == 2) {
+        static_assert(KLEV == 0, "CIOS interleaves reduction and product rows: schoolbook only");
+        cios_op<C>(NB, X, B, mode == MODE_REDC, N, NP, T, Q, OUT);
+    } else {
+        mont_op_k<C, RM == 1, KLEV>(mode, NB, X, B, N, NP, T, Q, OUT, KS, sg);
+    }
+}
+
 }  // namespace mpb

@@ -334,6 +334,99 @@ MPB_DEVI void mont_op(int mode, int NB, const Arr& X, const Arr& B, const Arr& N
     }
 }
 
+// ------------------------------------------------- CIOS (third REDC mode)
+// alg:8BlockMontRed, the CIOS-inspired interleaved Montgomery multiplication, with
+// the paper's machine word (52 bits, one VPMADD52 lane) replaced by the engine's block of C limbs:
+// digit d = 2^{32C}, m_i = (Y mod d) * N' mod d (only the low block of N', the block analog of
+// n0'), then Y <- (Y + m_i N) / d.  Per row i the block pass t = 0..NB-1 computes
+//   Z_t = carry + Y_t + a_i B_t + m_i N_t,  Y_{t-1} <- Z_t mod d,  carry <- Z_t / d
+// (block 0 of Z vanishes by the choice of m_i).  Y < 2N throughout, so Y has L limbs plus a top
+// bit; the result is canonicalised by one masked conditional subtraction.  B_ONE: B = 1 (used
+// for REDC(X) = MontMul(X, 1) in the exponentiation).  Scratch: Y (L limbs), M (C limbs).
+template <int C>
+MPB_DEVI void cios_op(int NB, const Arr& X, const Arr& B, bool b_one, const Arr& N, const Arr& NP, const Arr& Y,
+                      const Arr& M, const Arr& OUT) {
+    uint32_t ytop = 0;
+#pragma unroll 1
+    for (int i = 0; i < NB; i++) {
+        uint32_t W[2 * C + 1];
+        w_zero<C>(W);
+#pragma unroll 1
+        for (int t = 0; t < NB; t++) {
+            if (i > 0) {  // + Y_t (Y = 0 before the first row)
+                uint32_t yt[C];
+                ldb<C>(Y, t, yt);
+                w_add<0, C, 0>(W, yt);
+            }
+            {  // + a_i * B_t
+                uint32_t x[C], y[C];
+                ldb<C>(X, i, x);
+                if (b_one) {
+#pragma unroll
+                    for (int k = 0; k < C; k++) y[k] = 0;
+                    y[0] = t == 0 ? 1u : 0u;
+                } else {
+                    ldb<C>(B, t, y);
+                }
+                acc_mul<C>(W, x, y);
+            }
+            if (t == 0) {  // m_i = (Z mod d) * N' mod d  (low-half block product)
+                uint32_t z[C], np[C], E[2 * C], O[2 * C];
+#pragma unroll
+                for (int k = 0; k < C; k++) z[k] = W[k];
+                ldb<C>(NP, 0, np);
+                bp_lo<C>(z, np, E, O);
+                uint32_t m[C];
+#pragma unroll
+                for (int k = 0; k < C; k++) m[k] = E[k];
+                w_add_trunc<1, C - 1, 0>(m, O);
+                stb<C>(M, 0, m);
+            }
+            {  // + m_i * N_t
+                uint32_t m[C], n[C];
+                ldb<C>(M, 0, m);
+                ldb<C>(N, t, n);
+                acc_mul<C>(W, m, n);
+            }
+            if (t > 0) stb<C>(Y, t - 1, W);  // block 0 of Z_0 is zero
+            w_shift<C>(W);
+        }
+        // W[0..C] = the top of Z (positions L .. L+C); add the old top bit of Y at position L
+        add_first(W[0], ytop);
+#pragma unroll
+        for (int k = 1; k <= C; k++) add_next(W[k], 0u);
+        stb<C>(Y, NB - 1, W);
+        ytop = W[C];
+    }
+    // canonical: OUT = (ytop || Y >= N) ? Y - N : Y, by a mask
+    uint32_t borrow = 0;
+#pragma unroll 1
+    for (int j = 0; j < NB; j++) {
+        uint32_t c[C], n[C];
+        ldb<C>(Y, j, c);
+        ldb<C>(N, j, n);
+        bc_restore(borrow);
+#pragma unroll
+        for (int k = 0; k < C; k++) sub_next(c[k], n[k]);
+        borrow = bc_save();
+        stb<C>(OUT, j, c);
+    }
+    const uint32_t msk = 0u - ((ytop | (borrow ^ 1u)) & 1u);
+#pragma unroll 1
+    for (int j = 0; j < NB; j++) {
+#pragma unroll
+        for (int q = 0; q < C / 4; q++) {
+            uint4 d = OUT.ld(j * (C / 4) + q);
+            const uint4 y = Y.ld(j * (C / 4) + q);
+            d.x = (d.x & msk) | (y.x & ~msk);
+            d.y = (d.y & msk) | (y.y & ~msk);
+            d.z = (d.z & msk) | (y.z & ~msk);
+            d.w = (d.w & msk) | (y.w & ~msk);
+            OUT.st(j * (C / 4) + q, d);
+        }
+    }
+}
+
 // ---------------------------------------------------------- CT table select
 // OUT = G[idx] by a masked scan of every entry ("constant-time batch selection").
 // Entry e, chunk q lives at chunk index e*(L/4) + q of G.  The scan is bound by DRAM latency

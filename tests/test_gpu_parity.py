@@ -25,7 +25,8 @@ BITS_MOD = [512, 1024, 2048, 3072, 4096, 4108]
 BITS_ODD = [256, 700, 1536]  # block sizes 8 and 12, odd block counts
 BITS_MUL = [512, 1024, 2048, 3072, 4096, 4154]
 ALGOS = [1, 2, 3]  # schoolbook, 1-level Karatsuba, 2-level Karatsuba
-REDC = [1, 0]  # truncated, full
+REDC = [1, 0, 2]  # truncated, full, CIOS (alg:8BlockMontRed)
+REDC_STANDALONE = [1, 0]  # a stand-alone REDC has no CIOS form
 
 
 @pytest.fixture(scope="module")
@@ -125,7 +126,7 @@ def test_mont_mul_sqr(mpb, bits, redc):
 
 
 # --------------------------------------------------------------------- REDC
-@pytest.mark.parametrize("redc", REDC)
+@pytest.mark.parametrize("redc", REDC_STANDALONE)
 @pytest.mark.parametrize("bits", BITS_MOD + BITS_ODD)
 def test_mont_redc_adversarial(mpb, bits, redc):
     """The exact carry correction of Theorem 2 (families alpha..delta, tests/adversarial.py)."""
@@ -228,6 +229,8 @@ def test_config3_full_batch_sampled(mpb):
     out_t = mpb.mont_batch_modexp_ct(dN, Np, R2, dB, dE, bits, 5, redc=1, ws=ws)
     out_f = mpb.mont_batch_modexp_ct(dN, Np, R2, dB, dE, bits, 5, redc=0, ws=ws)
     assert torch.equal(out_t, out_f)
+    out_c = mpb.mont_batch_modexp_ct(dN, Np, R2, dB, dE, bits, 5, redc=2, ws=ws)
+    assert torch.equal(out_t, out_c)
     h = mpb.to_host(out_t)
     idx = np.random.default_rng(3).choice(count, size=48, replace=False)
     idx = np.concatenate([idx, [0, count - 1]])
@@ -247,6 +250,10 @@ def test_abi_errors_and_noop(mpb):
         mpb.mont_batch_mul(da, da, dN, Np, bits, redc=5)
     with pytest.raises(ValueError):
         mpb.mp_batch_mul(da, da, 20000)  # beyond the 16384-bit maximum
+    with pytest.raises(ValueError):  # CIOS has no stand-alone REDC form
+        mpb.mont_batch_redc(mpb.to_device(np.zeros((4, 64), np.uint32)), dN, Np, bits, redc=2)
+    with pytest.raises(ValueError):  # CIOS interleaves schoolbook rows: no Karatsuba
+        mpb.mont_batch_modexp_ct(dN, Np, R2, da, da, bits, redc=2, algo=2)
     assert not mpb.supported(20000) and mpb.supported(700) and mpb.supported(2048) and mpb.supported(4108)
     # count == 0 is a no-op
     z = mpb.empty_sliced(32, 0)
