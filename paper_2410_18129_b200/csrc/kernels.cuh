@@ -19,7 +19,13 @@ constexpr int kThreads = 128;
 
 // resident CTAs per SM the heavy kernels are compiled for (register budget 65536 / (128 * minb))
 template <int C>
-__host__ __device__ constexpr int min_blocks() { return C >= 12 ? 3 : 5; }
+__host__ __device__ constexpr int min_blocks() {
+#ifdef MPB_MINB
+    return MPB_MINB;
+#else
+    return C >= 12 ? 3 : 5;
+#endif
+}
 // entries of the CT table scan kept in flight per step (x 4 chunks); measured best at L = 64
 template <int C>
 __host__ __device__ constexpr int select_unroll() {

@@ -160,6 +160,9 @@ MPB_DEVI void engine(int ph, int NB, const Arr& AX, const Arr& AY, const Arr& DS
     uint32_t W[2 * C + 1];
     w_zero<C>(W);
     uint32_t carry = 0, borrow = 0;
+    const bool sqr = ph == PH_SQR;
+    const bool hi_trunc = TRUNC && ph == PH_HI;
+    // block columns k0 .. k1-1; pairs (k, s) with s in [max(0, k-NB+1), min(k, NB-1)] (SQR: s <= k/2)
     int k0 = 0, k1 = 2 * NB - 1;
     if (ph == PH_Q) k1 = NB;
     if (ph == PH_HI) {
@@ -176,142 +179,138 @@ MPB_DEVI void engine(int ph, int NB, const Arr& AX, const Arr& AY, const Arr& DS
                              : "+r"(W[0]), "+r"(W[1]) : "r"(qv.w), "r"(nv.w));
             }
             orlo = 0u - tl1 - b;  // reuse: K = (-T[L-1] - b) mod 2^32
-        } else {
-            k1 = 2 * NB;
         }
+        // FULL: k1 = 2NB-1 here; the empty top column 2NB-1 is finished after the loop
     }
-    // pair (k, s) ranges of block column k; pairs are prefetched one ahead into shared memory
-    auto s_lo_of = [&](int k) { return k - NB + 1 > 0 ? k - NB + 1 : 0; };
-    auto s_hi_of = [&](int k) {
-        int h = k < NB - 1 ? k : NB - 1;
-        if (ph == PH_SQR) h = k >> 1;
-        return h;
-    };
-    auto advance = [&](int& k, int& s) -> bool {  // next pair after (k, s), false if none
-        if (s < s_hi_of(k)) {
-            s++;
-            return true;
-        }
-#pragma unroll 1
-        for (k = k + 1; k < k1; k++) {
-            s = s_lo_of(k);
-            if (s <= s_hi_of(k)) return true;
-        }
-        return false;
-    };
-    auto issue = [&](int k, int s, int buf) {
+    // One linear walk over the pairs: (k, s) is the pair being computed, (nk, ns) the next one,
+    // whose operand blocks are prefetched (cp.async, double buffered) while (k, s) runs.
+    const char* const axp = AX.p;
+    const char* const ayp = AY.p;
+    const uint32_t sb = AX.sb;
+    auto issue = [&](int kk, int ss, int buf) {
         const uint32_t b = sg.base + (uint32_t)(buf * 2 * (C / 4)) * sg.cs;
+        const uint32_t cx = (uint32_t)ss * (C / 4), cy = (uint32_t)(kk - ss) * (C / 4);
 #pragma unroll
-        for (int q = 0; q < C / 4; q++) cp_async16(b + q * sg.cs, AX.addr(s * (C / 4) + q));
-        if (!(ph == PH_SQR && 2 * s == k)) {
+        for (int q = 0; q < C / 4; q++) cp_async16(b + q * sg.cs, axp + (size_t)(cx + q) * sb);
+        if (!(sqr && 2 * ss == kk)) {
 #pragma unroll
-            for (int q = 0; q < C / 4; q++) cp_async16(b + (C / 4 + q) * sg.cs, AY.addr((k - s) * (C / 4) + q));
+            for (int q = 0; q < C / 4; q++) cp_async16(b + (C / 4 + q) * sg.cs, ayp + (size_t)(cy + q) * sb);
         }
         cp_commit();
     };
-    {
-        int fk = k0, fs = s_lo_of(k0) - 1;
-        if (k0 < k1 && s_lo_of(k0) <= s_hi_of(k0)) fs = s_lo_of(k0);
-        else if (!advance(fk, fs)) fk = -1;
-        if (fk >= 0) issue(fk, fs, 0);
-    }
+    int k = k0, s = k0 - NB + 1 > 0 ? k0 - NB + 1 : 0;
+    int s_hi = sqr ? (k >> 1) : (k < NB - 1 ? k : NB - 1);
+    issue(k, s, 0);
     int buf = 0;
 #pragma unroll 1
-    for (int k = k0; k < k1; k++) {
-        const int s_lo = s_lo_of(k);
-        const int s_hi = s_hi_of(k);
-#pragma unroll 1
-        for (int s = s_lo; s <= s_hi; s++) {
-            const int t = k - s;
-            int op = OP_MUL;
-            if (ph == PH_SQR) op = s < t ? OP_MUL2 : OP_SQR;
-            else if (ph == PH_Q && k == NB - 1) op = OP_LO;
-            else if (ph == PH_HI && TRUNC && k == NB - 1) op = OP_HI;
-            {
-                int nk = k, ns = s;
-                if (advance(nk, ns)) {
-                    issue(nk, ns, buf ^ 1);
-                    cp_wait<1>();
-                } else {
-                    cp_wait<0>();
-                }
+    while (k < k1) {
+        // next pair
+        int nk = k, ns = s + 1, ns_hi = s_hi;
+        if (ns > s_hi) {
+            nk = k + 1;
+            ns = nk - NB + 1 > 0 ? nk - NB + 1 : 0;
+            ns_hi = sqr ? (nk >> 1) : (nk < NB - 1 ? nk : NB - 1);
+        }
+        const bool more = nk < k1;
+        if (more) {
+            issue(nk, ns, buf ^ 1);
+            cp_wait<1>();
+        } else {
+            cp_wait<0>();
+        }
+        const int t = k - s;
+        const bool diag = sqr && s == t;
+        uint32_t x[C], y[C];
+        {
+            const uint32_t b = sg.base + (uint32_t)(buf * 2 * (C / 4)) * sg.cs;
+#pragma unroll
+            for (int q = 0; q < C / 4; q++) {
+                const uint4 v = lds128(b + q * sg.cs);
+                x[4 * q] = v.x; x[4 * q + 1] = v.y; x[4 * q + 2] = v.z; x[4 * q + 3] = v.w;
             }
-            uint32_t x[C], y[C];
-            {
-                const uint32_t b = sg.base + (uint32_t)(buf * 2 * (C / 4)) * sg.cs;
+            if (!diag) {
 #pragma unroll
                 for (int q = 0; q < C / 4; q++) {
-                    const uint4 v = lds128(b + q * sg.cs);
-                    x[4 * q] = v.x; x[4 * q + 1] = v.y; x[4 * q + 2] = v.z; x[4 * q + 3] = v.w;
-                }
-                if (op != OP_SQR) {
-#pragma unroll
-                    for (int q = 0; q < C / 4; q++) {
-                        const uint4 v = lds128(b + (C / 4 + q) * sg.cs);
-                        y[4 * q] = v.x; y[4 * q + 1] = v.y; y[4 * q + 2] = v.z; y[4 * q + 3] = v.w;
-                    }
+                    const uint4 v = lds128(b + (C / 4 + q) * sg.cs);
+                    y[4 * q] = v.x; y[4 * q + 1] = v.y; y[4 * q + 2] = v.z; y[4 * q + 3] = v.w;
                 }
             }
-            buf ^= 1;
-            if (ph == PH_Q && s == k) {  // block T_k is loaded with t == 0 exactly once
+        }
+        buf ^= 1;
+        if (ph == PH_Q && t == 0) {  // block T_k is loaded with t == 0 exactly once
 #pragma unroll
-                for (int i = 0; i < C - 1; i++) orlo |= x[i];
-                if (k == NB - 1) tl1 = x[C - 1];
-                else orlo |= x[C - 1];
-            }
-            if (op == OP_SQR) {
-                acc_sqr<C>(W, x);
-            } else if (op == OP_LO) {
-                acc_lo<C>(W, x, y);
-            } else if (op == OP_HI) {
-                acc_hi<C>(W, x, y);
-            } else {
-                uint32_t E[2 * C], O[2 * C];
-                bp_mul<C>(x, y, E, O);
+            for (int i = 0; i < C - 1; i++) orlo |= x[i];
+            if (k == NB - 1) tl1 = x[C - 1];
+            else orlo |= x[C - 1];
+        }
+        const bool lo_col = ph == PH_Q && k == NB - 1;
+        const bool hi_col = hi_trunc && k == NB - 1;
+        if (diag) {
+            acc_sqr<C>(W, x);
+        } else if (lo_col) {
+            acc_lo<C>(W, x, y);
+        } else if (hi_col) {
+            acc_hi<C>(W, x, y);
+        } else {
+            uint32_t E[2 * C], O[2 * C];
+            bp_mul<C>(x, y, E, O);
+            w_add<0, 2 * C, 0>(W, E);
+            w_add<1, 2 * C - 1, 0>(W, O);
+            if (sqr) {  // s < t: the product counts twice
                 w_add<0, 2 * C, 0>(W, E);
                 w_add<1, 2 * C - 1, 0>(W, O);
-                if (op == OP_MUL2) {
-                    w_add<0, 2 * C, 0>(W, E);
-                    w_add<1, 2 * C - 1, 0>(W, O);
-                }
             }
         }
-        // ---- end of block column k
-        if (ph != PH_HI) {
-            stb<C>(DST, k, W);
-            w_shift<C>(W);
-        } else if (TRUNC) {
-            if (k == NB - 1) {
-                // exact carry out of column L-1: floor(S/2^32) + [S mod 2^32 > K]
-                const uint32_t corr = W[0] > orlo ? 1u : 0u;
+        if (nk != k) {  // ---- end of block column k
+            if (ph != PH_HI) {
+                stb<C>(DST, k, W);
+                w_shift<C>(W);
+            } else if (TRUNC) {
+                if (k == NB - 1) {
+                    // exact carry out of column L-1: floor(S/2^32) + [S mod 2^32 > K]
+                    const uint32_t corr = W[0] > orlo ? 1u : 0u;
 #pragma unroll
-                for (int i = 0; i < 2 * C; i++) W[i] = W[i + 1];
-                W[2 * C] = 0;
-                add_first(W[0], corr);
+                    for (int i = 0; i < 2 * C; i++) W[i] = W[i + 1];
+                    W[2 * C] = 0;
+                    add_first(W[0], corr);
 #pragma unroll
-                for (int i = 1; i <= C; i++) add_next(W[i], 0u);
-                absorb(W[C + 1]);
+                    for (int i = 1; i <= C; i++) add_next(W[i], 0u);
+                    absorb(W[C + 1]);
+                } else {
+                    emit_block<C>(W, k - NB, NB, true, T, N, OUT, carry, borrow);
+                    w_shift<C>(W);
+                }
             } else {
-                emit_block<C>(W, k - NB, NB, true, T, N, OUT, carry, borrow);
+                uint32_t tb[C];  // + T block k, carried through the whole window
+                ldb<C>(T, k, tb);
+                add_first(W[0], tb[0]);
+#pragma unroll
+                for (int i = 1; i < C; i++) add_next(W[i], tb[i]);
+#pragma unroll
+                for (int i = C; i < 2 * C; i++) add_next(W[i], 0u);
+                absorb(W[2 * C]);
+                if (k >= NB) emit_block<C>(W, k - NB, NB, false, T, N, OUT, carry, borrow);
                 w_shift<C>(W);
             }
-        } else {
-            uint32_t tb[C];  // + T block k, carried through the whole window
-            ldb<C>(T, k, tb);
-            add_first(W[0], tb[0]);
-#pragma unroll
-            for (int i = 1; i < C; i++) add_next(W[i], tb[i]);
-#pragma unroll
-            for (int i = C; i < 2 * C; i++) add_next(W[i], 0u);
-            absorb(W[2 * C]);
-            if (k >= NB) emit_block<C>(W, k - NB, NB, false, T, N, OUT, carry, borrow);
-            w_shift<C>(W);
         }
+        k = nk;
+        s = ns;
+        s_hi = ns_hi;
     }
     if (ph == PH_MUL || ph == PH_SQR) stb<C>(DST, 2 * NB - 1, W);
     if (ph == PH_HI) {
-        if (TRUNC) emit_block<C>(W, NB - 1, NB, true, T, N, OUT, carry, borrow);
-        final_select<C>(NB, T, OUT, TRUNC ? carry : W[0], borrow);
+        if (TRUNC) {
+            emit_block<C>(W, NB - 1, NB, true, T, N, OUT, carry, borrow);
+        } else {  // empty top column 2NB-1: + T block 2NB-1, emit the last block of C
+            uint32_t tb[C];
+            ldb<C>(T, 2 * NB - 1, tb);
+            add_first(W[0], tb[0]);
+#pragma unroll
+            for (int i = 1; i < C; i++) add_next(W[i], tb[i]);
+            add_next(W[C], 0u);
+            emit_block<C>(W, NB - 1, NB, false, T, N, OUT, carry, borrow);
+        }
+        final_select<C>(NB, T, OUT, TRUNC ? carry : W[C], borrow);
     }
 }
 
