@@ -58,6 +58,7 @@ def lib():
             "o_montred_classic": (i, [_u32p, _u32p, _u32p, i, _u32p]),
             "o_montred_truncated": (i, [_u32p, _u32p, _u32p, i, _u32p, _u32p]),
             "o_montmul_cios": (i, [_u32p, _u32p, _u32p, ctypes.c_uint32, i, _u32p]),
+            "o_rsa_crt": (i, [_u32p, _u32p, _u32p, _u32p, _u32p, _u32p, i, i, _u32p]),
             "o_batch_modexp": (i, [_u32p, _u32p, i, _u32p, i, _u32p, sz, i]),
             "o_batch_montmul": (i, [_u32p, _u32p, _u32p, i, _u32p, sz, i]),
         }
@@ -190,6 +191,15 @@ def montmul_cios(a: int, b: int, N: int, n0p: int, L: int) -> int:
     if lib().o_montmul_cios(_p(A), _p(B), _p(Nn), n0p, L, _p(C)) != 0:
         raise ValueError("a low word of Y + q*N did not vanish")
     return from_limbs(C)
+
+
+def rsa_crt(c: int, p: int, q: int, dp: int, dq: int, qinv: int, Lh: int, ebits: int) -> int:
+    """CRT-RSA private-key operation (Garner), step by step: m = c^d mod pq."""
+    m = np.zeros(2 * Lh, np.uint32)
+    args = [_arr(c, 2 * Lh), _arr(p, Lh), _arr(q, Lh), _arr(dp, Lh), _arr(dq, Lh), _arr(qinv, Lh)]
+    if lib().o_rsa_crt(*[_p(a) for a in args], Lh, ebits, _p(m)) != 0:
+        raise ValueError("invalid CRT-RSA operands")
+    return from_limbs(m)
 
 
 # ---------------------------------------------------------- batch interface

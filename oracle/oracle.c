@@ -534,6 +534,54 @@ int o_montmul_cios(const uint32_t* a, const uint32_t* B, const uint32_t* N, uint
     return 0;
 }
 
+/* Batched CRT-RSA private-key operation (the paper's motivating use; SURVEY
+ * 8(f) f4), step by step with plain definitions (Garner recombination):
+ *   c_p = c mod p, c_q = c mod q;  m_p = c_p^dp mod p,  m_q = c_q^dq mod q;
+ *   h = qinv*(m_p - m_q) mod p;  m = m_q + h*q   (= c^d mod pq for d = dp mod p-1, dq mod q-1).
+ * c and m have 2*Lh limbs (c < p*q); p, q, dp, dq, qinv have Lh limbs; ebits = bits of dp, dq. */
+int o_rsa_crt(const uint32_t* c, const uint32_t* p, const uint32_t* q, const uint32_t* dp, const uint32_t* dq,
+              const uint32_t* qinv, int Lh, int ebits, uint32_t* m) {
+    const size_t H = (size_t)Lh;
+    uint32_t* cp = zalloc(H);
+    uint32_t* cq = zalloc(H);
+    uint32_t* mp = zalloc(H);
+    uint32_t* mq = zalloc(H);
+    uint32_t* w = zalloc(2 * H);
+    uint32_t* t = zalloc(H + 1);
+    uint32_t* d = zalloc(H + 1);
+    uint32_t* h = zalloc(H);
+    int rc = 0;
+    rc |= o_divmod(c, 2 * Lh, p, Lh, NULL, cp);
+    rc |= o_divmod(c, 2 * Lh, q, Lh, NULL, cq);
+    rc |= o_modexp(cp, dp, ebits, p, Lh, mp);
+    rc |= o_modexp(cq, dq, ebits, q, Lh, mq);
+    /* t = m_q mod p */
+    memcpy(w, mq, sizeof(uint32_t) * H);
+    memset(w + H, 0, sizeof(uint32_t) * H);
+    rc |= o_divmod(w, 2 * Lh, p, Lh, NULL, t);
+    /* d = (m_p - t) mod p, in [0, p) */
+    memcpy(d, mp, sizeof(uint32_t) * H);
+    d[H] = 0;
+    t[H] = 0;
+    if (bn_cmp(d, Lh + 1, t, Lh + 1) < 0) {
+        uint32_t* pw = zalloc(H + 1);
+        memcpy(pw, p, sizeof(uint32_t) * H);
+        bn_add(d, d, pw, Lh + 1);
+        free(pw);
+    }
+    bn_sub(d, d, t, Lh + 1);
+    /* h = qinv * d mod p */
+    o_mul(qinv, Lh, d, Lh, w);
+    rc |= o_divmod(w, 2 * Lh, p, Lh, NULL, h);
+    /* m = m_q + h*q  (< p*q: no reduction) */
+    o_mul(h, Lh, q, Lh, w);
+    uint32_t* mq2 = zalloc(2 * H);
+    memcpy(mq2, mq, sizeof(uint32_t) * H);
+    bn_add(m, w, mq2, 2 * Lh);
+    free(mq2); free(cp); free(cq); free(mp); free(mq); free(w); free(t); free(d); free(h);
+    return rc ? -1 : 0;
+}
+
 /* ------------------------------------------------------ batch drivers */
 
 typedef struct {

@@ -64,6 +64,12 @@ int o_montred_truncated(const uint32_t* T, const uint32_t* N, const uint32_t* Np
  * C = a*B*R^-1 mod N up to one N (C < 2N), L+1 limbs; -1 if a low word fails to vanish. */
 int o_montmul_cios(const uint32_t* a, const uint32_t* B, const uint32_t* N, uint32_t n0p, int L, uint32_t* C);
 
+/* Batched CRT-RSA private-key operation: c_p = c mod p, c_q = c mod q,
+ * m_p = c_p^dp mod p, m_q = c_q^dq mod q, h = qinv*(m_p - m_q) mod p, m = m_q + h*q.
+ * c, m: 2*Lh limbs; p, q, dp, dq, qinv: Lh limbs; ebits = exponent bits of dp, dq. */
+int o_rsa_crt(const uint32_t* c, const uint32_t* p, const uint32_t* q, const uint32_t* dp, const uint32_t* dq,
+              const uint32_t* qinv, int Lh, int ebits, uint32_t* m);
+
 /* ---- batch drivers (pthreads over independent items; operand-major arrays) ---- */
 int o_batch_modexp(const uint32_t* base, const uint32_t* e, int ebits, const uint32_t* N, int L,
                    uint32_t* out, size_t count, int threads);

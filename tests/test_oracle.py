@@ -314,6 +314,30 @@ def test_rsa_round_trip():
         assert O.modexp(c, d, n, L) == m
 
 
+@pytest.mark.parametrize("bits", [256, 1024])
+def test_rsa_crt_route(bits):
+    """CRT-RSA (Garner) step by step equals the full-size private-key power c^d mod n (Python pow
+    and the oracle's own modexp), including c = 0, 1, n-1 and c sharing a factor with n, and
+    inverts the public operation (m^e)^d = m."""
+    h = bits // 2
+    Lh = I.limbs_for_bits(h)
+    p, q = O.gen_prime(h, 2 * bits + 1), O.gen_prime(h, 2 * bits + 2)
+    n = p * q
+    lam = (p - 1) * (q - 1) // math.gcd(p - 1, q - 1)
+    e = 65537
+    d = O.inv_mod(e, lam)
+    dp, dq, qinv = d % (p - 1), d % (q - 1), O.inv_mod(q, p)
+    assert (qinv * q) % p == 1
+    cs = [0, 1, n - 1, p * 3, q * 5, RNG.randrange(n), RNG.randrange(n)]
+    for c in cs:
+        m = O.rsa_crt(c, p, q, dp, dq, qinv, Lh, h)
+        assert m == pow(c, d, n)
+        if bits <= 256:
+            assert m == O.modexp(c, d, n, I.limbs_for_bits(bits))
+    msg = RNG.randrange(n)
+    assert O.rsa_crt(pow(msg, e, n), p, q, dp, dq, qinv, Lh, h) == msg
+
+
 # ----------------------------------------------------------------- batch driver
 def test_batch_drivers_match_single_calls():
     N, base, exp = I.modexp_inputs(config=1, count=8, bits=1024)
