@@ -99,6 +99,19 @@ int mont_batch_setup(const uint32_t* N, uint32_t* Nprime, uint32_t* R2, size_t c
                      void* workspace, size_t workspace_bytes, void* stream);
 size_t mont_batch_setup_workspace(size_t count, int bits);
 
+/* Batched CRT-RSA private-key operation (the paper's motivating use, P:L20 / P:L28; SURVEY
+ * 8(f) f4): m = c^d mod pq computed as m_p = (c mod p)^dp mod p, m_q = (c mod q)^dq mod q by one
+ * constant-time exponentiation over the 2*count half-size operands, then Garner's recombination
+ * m = m_q + q * (qinv * (m_p - m_q) mod p).  bits = modulus size (even, >= 128); c and m have
+ * mpb_limbs(bits) limbs, p, q, dp, dq, qinv have mpb_limbs(bits/2) limbs (word-sliced, `count`
+ * operands each).  Preconditions (not checked on the device): p, q odd with exactly bits/2 bits,
+ * qinv = q^-1 mod p, c < p*q, dp, dq < 2^(bits/2).  redc selects the REDC mode of the
+ * exponentiation.  workspace: rsa_batch_crt_workspace(count, bits, window) bytes. */
+int rsa_batch_crt_ct(const uint32_t* c, const uint32_t* p, const uint32_t* q, const uint32_t* dp, const uint32_t* dq,
+                     const uint32_t* qinv, uint32_t* m, size_t count, int bits, int window, int redc,
+                     void* workspace, size_t workspace_bytes, void* stream);
+size_t rsa_batch_crt_workspace(size_t count, int bits, int window);
+
 /* End-to-end convenience over HOST buffers (operand-major, L limbs each; exp L limbs):
  * allocates device memory, copies in, runs setup + modexp, copies out, synchronises.
  * Returns MPB_OK or an error; blocking. */

@@ -299,6 +299,74 @@ int mont_batch_setup(const uint32_t* N, uint32_t* NP, uint32_t* R2, size_t count
     });
 }
 
+// ------------------------------------------------------------------ CRT-RSA
+// Layout of the CRT workspace (uint32 words; n2 = 2*count operands of Lh limbs, word-sliced):
+//   PQ | NPQ | R2Q | E | B | M   (6 * n2 * Lh)  then scratch shared by the steps.
+static size_t crt_scratch_words(size_t count, int bits, int window) {
+    const int h = bits / 2, Lh = mpb_limbs(h);
+    const size_t n2 = 2 * count;
+    size_t w = mont_batch_setup_workspace(n2, h) / 4;
+    const size_t me = mont_batch_modexp_ct_workspace(n2, h, window, MPB_ALGO_AUTO) / 4;
+    if (me > w) w = me;
+    if ((size_t)4 * Lh * n2 > w) w = (size_t)4 * Lh * n2;        // reduce: T, Q, X
+    if ((size_t)7 * Lh * count > w) w = (size_t)7 * Lh * count;  // recombine: T, Q, X, H, PR
+    return w;
+}
+
+size_t rsa_batch_crt_workspace(size_t count, int bits, int window) {
+    if (bits < 128 || (bits & 1) || window < 1 || window > 6) return 0;
+    const int Lh = mpb_limbs(bits / 2);
+    return (6 * (2 * count) * (size_t)Lh + crt_scratch_words(count, bits, window)) * sizeof(uint32_t);
+}
+
+int rsa_batch_crt_ct(const uint32_t* c, const uint32_t* p, const uint32_t* q, const uint32_t* dp, const uint32_t* dq,
+                     const uint32_t* qinv, uint32_t* m, size_t count, int bits, int window, int redc, void* ws,
+                     size_t ws_bytes, void* stream) {
+    g_err.clear();
+    if (!redc_ok(redc)) return fail(MPB_EINVAL, "redc out of range");
+    if (window < 1 || window > 6) return fail(MPB_EINVAL, "window must be in 1..6");
+    if (bits < 128 || (bits & 1)) return fail(MPB_EUNSUPPORTED, "bits must be even and >= 128");
+    int L, Lh;
+    if (int rc = limbs_checked(bits, L)) return rc;
+    if (int rc = limbs_checked(bits / 2, Lh)) return rc;
+    if (count == 0) return MPB_OK;
+    if (int rc = check_ptrs({c, p, q, dp, dq, qinv, m, ws})) return rc;
+    for (const void* in : {(const void*)c, (const void*)p, (const void*)q, (const void*)dp, (const void*)dq,
+                           (const void*)qinv})
+        if (in == m) return fail(MPB_EINVAL, "output aliases an input");
+    if (ws_bytes < rsa_batch_crt_workspace(count, bits, window)) return fail(MPB_EINVAL, "workspace too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int h = bits / 2;
+    const size_t n2 = 2 * count, arr_w = n2 * (size_t)Lh;
+    uint32_t* base = (uint32_t*)ws;
+    uint32_t *PQ = base, *NPQ = base + arr_w, *R2Q = base + 2 * arr_w, *E = base + 3 * arr_w, *B = base + 4 * arr_w,
+             *M = base + 5 * arr_w, *scr = base + 6 * arr_w;
+    const size_t scr_bytes = crt_scratch_words(count, bits, window) * sizeof(uint32_t);
+    // [p; q] and [dp; dq] as 2*count-operand word-sliced arrays: per 16-byte chunk row, count
+    // operands from each source (a pitched copy; no arithmetic)
+    auto concat = [&](const uint32_t* a, const uint32_t* b, uint32_t* dst) -> bool {
+        const size_t row = count * 16, drow = n2 * 16;
+        return cudaMemcpy2DAsync(dst, drow, a, row, row, Lh / 4, cudaMemcpyDeviceToDevice, s) == cudaSuccess &&
+               cudaMemcpy2DAsync((char*)dst + row, drow, b, row, row, Lh / 4, cudaMemcpyDeviceToDevice, s) ==
+                   cudaSuccess;
+    };
+    if (!concat(p, q, PQ) || !concat(dp, dq, E)) return fail(MPB_ECUDA, "device copy failed");
+    if (int rc = mont_batch_setup(PQ, NPQ, R2Q, n2, h, scr, scr_bytes, stream)) return rc;
+    int rc = dispatch_L(Lh, [&](auto Ci, int nb) {
+        constexpr int C = decltype(Ci)::value;
+        Launch<C>::crt_reduce(c, L, PQ, NPQ, R2Q, B, count, nb, scr, s);
+        return check_launch();
+    });
+    if (rc) return rc;
+    if ((rc = mont_batch_modexp_ct(PQ, NPQ, R2Q, B, E, M, n2, h, window, redc, MPB_ALGO_AUTO, scr, scr_bytes, stream)))
+        return rc;
+    return dispatch_L(Lh, [&](auto Ci, int nb) {
+        constexpr int C = decltype(Ci)::value;
+        Launch<C>::crt_recombine(M, PQ, NPQ, R2Q, qinv, m, L, count, nb, scr, s);
+        return check_launch();
+    });
+}
+
 int mpb_modexp_host(const uint32_t* N, const uint32_t* base, const uint32_t* exp, uint32_t* out, size_t count,
                     int bits, int window, int redc, void* stream) {
     g_err.clear();

@@ -203,6 +203,138 @@ __global__ void __launch_bounds__(kThreads) k_setup(const uint32_t* __restrict__
                  word_at(N, count, k, 0), nbits);
 }
 
+// ------------------------------------------------------------------ CRT-RSA
+// Batched CRT-RSA private-key operation (the paper's motivating use; SURVEY
+// 8(f) f4): three launches around the half-size exponentiation.  Arrays of n2 = 2*count operands
+// hold the p-items at 0..count-1 and the q-items at count..2count-1 (word-sliced, stride n2).
+//   k_crt_reduce    B_j = c mod P_j = MontMul(REDC(c), R^2 mod P_j)   (REDC needs c < P_j * R)
+//   (modexp)        M_j = B_j^E_j mod P_j                              (mont_batch_modexp_ct)
+//   k_crt_recombine m = m_q + q * (qinv * (m_p - m_q) mod p)           (Garner)
+// Every step is a fixed sequence of block operations and masked selects (constant time).
+template <int C>
+__global__ void __launch_bounds__(kThreads) k_crt_reduce(const uint32_t* __restrict__ c, int Lc,
+                                                         const uint32_t* __restrict__ PQ, const uint32_t* __restrict__ NPQ,
+                                                         const uint32_t* __restrict__ R2Q, uint32_t* __restrict__ B,
+                                                         size_t count, int nb, uint32_t* ws) {
+    const size_t n2 = 2 * count;
+    const size_t j = tid_global();
+    if (j >= n2) return;
+    const size_t k = j < count ? j : j - count;
+    const int Lh = C * nb;
+    const Arr T = arr(ws, n2, j), Q = arr(ws + (size_t)2 * Lh * n2, n2, j), X = arr(ws + (size_t)3 * Lh * n2, n2, j);
+    const Arr Cc = arr(c, count, k);
+#pragma unroll 1
+    for (int q = 0; q < 2 * Lh / 4; q++) T.st(q, q < Lc / 4 ? Cc.ld(q) : make_uint4(0, 0, 0, 0));
+    const Arr N = arr(PQ, n2, j), NP = arr(NPQ, n2, j);
+    const Stage sg = stage();
+    mont_op<C, true>(MODE_REDC, nb, T, T, N, NP, T, Q, X, sg);                    // X = c R^-1 mod P_j
+    mont_op<C, true>(MODE_MUL, nb, X, arr(R2Q, n2, j), N, NP, T, Q, arr(B, n2, j), sg);  // B = c mod P_j
+}
+
+template <int C>
+__global__ void __launch_bounds__(kThreads) k_crt_recombine(const uint32_t* __restrict__ M, const uint32_t* __restrict__ PQ,
+                                                            const uint32_t* __restrict__ NPQ, const uint32_t* __restrict__ R2Q,
+                                                            const uint32_t* __restrict__ qinv, uint32_t* __restrict__ out,
+                                                            int Lo, size_t count, int nb, uint32_t* ws) {
+    const size_t k = tid_global();
+    if (k >= count) return;
+    const size_t n2 = 2 * count;
+    const int Lh = C * nb;
+    const Arr mp = arr(M, n2, k), mq = arr(M, n2, count + k), P = arr(PQ, n2, k), Qm = arr(PQ, n2, count + k);
+    const Arr NPp = arr(NPQ, n2, k), R2p = arr(R2Q, n2, k), QI = arr(qinv, count, k);
+    uint32_t* w = ws;
+    const Arr T = arr(w, count, k);
+    w += (size_t)2 * Lh * count;
+    const Arr Qs = arr(w, count, k);
+    w += (size_t)Lh * count;
+    const Arr X = arr(w, count, k);
+    w += (size_t)Lh * count;
+    const Arr H = arr(w, count, k);
+    w += (size_t)Lh * count;
+    const Arr PR = arr(w, count, k);  // 2Lh limbs
+    const Stage sg = stage();
+    // X = m_q - p; then X = borrow ? m_q : X   (m_q < q < 2p, so m_q mod p needs one subtraction)
+    uint32_t bw = 0;
+#pragma unroll 1
+    for (int b = 0; b < nb; b++) {
+        uint32_t u[C], v[C];
+        ldb<C>(mq, b, u);
+        ldb<C>(P, b, v);
+        bc_restore(bw);
+#pragma unroll
+        for (int i = 0; i < C; i++) sub_next(u[i], v[i]);
+        bw = bc_save();
+        stb<C>(X, b, u);
+    }
+    {
+        const uint32_t keep = 0u - bw;  // all ones: m_q < p, keep m_q
+#pragma unroll 1
+        for (int b = 0; b < nb; b++) {
+            uint32_t u[C], v[C];
+            ldb<C>(X, b, u);
+            ldb<C>(mq, b, v);
+#pragma unroll
+            for (int i = 0; i < C; i++) u[i] = (v[i] & keep) | (u[i] & ~keep);
+            stb<C>(X, b, u);
+        }
+    }
+    // X = m_p - X; if that borrowed, X += p
+    bw = 0;
+#pragma unroll 1
+    for (int b = 0; b < nb; b++) {
+        uint32_t u[C], v[C];
+        ldb<C>(mp, b, u);
+        ldb<C>(X, b, v);
+        bc_restore(bw);
+#pragma unroll
+        for (int i = 0; i < C; i++) sub_next(u[i], v[i]);
+        bw = bc_save();
+        stb<C>(X, b, u);
+    }
+    {
+        const uint32_t addp = 0u - bw;
+        uint32_t cy = 0;
+#pragma unroll 1
+        for (int b = 0; b < nb; b++) {
+            uint32_t u[C], v[C];
+            ldb<C>(X, b, u);
+            ldb<C>(P, b, v);
+            cc_restore(cy);
+#pragma unroll
+            for (int i = 0; i < C; i++) add_next(u[i], v[i] & addp);
+            cy = cc_save();
+            stb<C>(X, b, u);
+        }
+    }
+    mont_op<C, true>(MODE_MUL, nb, X, QI, P, NPp, T, Qs, H, sg);   // H = d qinv R^-1 mod p
+    mont_op<C, true>(MODE_MUL, nb, H, R2p, P, NPp, T, Qs, X, sg);  // X = h = d qinv mod p
+    {
+        uint32_t orlo = 0, tl1 = 0;
+        engine<C, true>(PH_MUL, nb, X, Qm, PR, PR, PR, PR, orlo, tl1, sg);  // PR = h q (2Lh limbs)
+    }
+    // out = PR + m_q  (< p q: the top 2Lh - Lo limbs are zero)
+    const Arr O = arr(out, count, k);
+    uint32_t cy = 0;
+#pragma unroll 1
+    for (int b = 0; b < 2 * nb; b++) {
+        uint32_t u[C], v[C];
+        ldb<C>(PR, b, u);
+        if (b < nb) {
+            ldb<C>(mq, b, v);
+        } else {
+#pragma unroll
+            for (int i = 0; i < C; i++) v[i] = 0;
+        }
+        cc_restore(cy);
+#pragma unroll
+        for (int i = 0; i < C; i++) add_next(u[i], v[i]);
+        cy = cc_save();
+#pragma unroll
+        for (int q = 0; q < C / 4; q++)
+            if ((b * C) / 4 + q < Lo / 4) O.st((b * C) / 4 + q, make_uint4(u[4 * q], u[4 * q + 1], u[4 * q + 2], u[4 * q + 3]));
+    }
+}
+
 // ---------------------------------------------------------------- launchers
 template <int C>
 void Launch<C>::setup(const uint32_t* N, uint32_t* NP, uint32_t* R2, size_t count, int nb, uint32_t* ws,
@@ -267,6 +399,18 @@ void Launch<C>::mont_mul(const uint32_t* a, const uint32_t* b, const uint32_t* N
         else if (redc == 1) go(std::integral_constant<int, 1>{});
         else go(std::integral_constant<int, 0>{});
     });
+}
+template <int C>
+void Launch<C>::crt_reduce(const uint32_t* c, int Lc, const uint32_t* PQ, const uint32_t* NPQ, const uint32_t* R2Q,
+                           uint32_t* B, size_t count, int nb, uint32_t* ws, cudaStream_t s) {
+    k_crt_reduce<C><<<grid_for(2 * count), kThreads, stage_bytes<C>(), s>>>(c, Lc, PQ, NPQ, R2Q, B, count, nb, ws);
+}
+template <int C>
+void Launch<C>::crt_recombine(const uint32_t* M, const uint32_t* PQ, const uint32_t* NPQ, const uint32_t* R2Q,
+                              const uint32_t* qinv, uint32_t* out, int Lo, size_t count, int nb, uint32_t* ws,
+                              cudaStream_t s) {
+    k_crt_recombine<C><<<grid_for(count), kThreads, stage_bytes<C>(), s>>>(M, PQ, NPQ, R2Q, qinv, out, Lo, count, nb,
+                                                                          ws);
 }
 template <int C>
 void Launch<C>::mont_redc(const uint32_t* T, const uint32_t* N, const uint32_t* NP, uint32_t* c, size_t count, int nb,

@@ -19,6 +19,12 @@ struct Launch {
                          size_t count, int nb, int redc, bool sqr, uint32_t* ws, cudaStream_t s);
     static void mont_redc(const uint32_t* T, const uint32_t* N, const uint32_t* NP, uint32_t* c, size_t count, int nb,
                           bool trunc, uint32_t* ws, cudaStream_t s);
+    // CRT-RSA (k_crt_reduce / k_crt_recombine in kernels.cuh); nb = blocks of the half size
+    static void crt_reduce(const uint32_t* c, int Lc, const uint32_t* PQ, const uint32_t* NPQ, const uint32_t* R2Q,
+                           uint32_t* B, size_t count, int nb, uint32_t* ws, cudaStream_t s);
+    static void crt_recombine(const uint32_t* M, const uint32_t* PQ, const uint32_t* NPQ, const uint32_t* R2Q,
+                              const uint32_t* qinv, uint32_t* out, int Lo, size_t count, int nb, uint32_t* ws,
+                              cudaStream_t s);
     // N' = (-N)^-1 mod R and R^2 mod N; ws: 6L words per operand
     static void setup(const uint32_t* N, uint32_t* NP, uint32_t* R2, size_t count, int nb, uint32_t* ws,
                       cudaStream_t s);

@@ -186,15 +186,15 @@ MPB_DEVI void engine(int ph, int NB, const Arr& AX, const Arr& AY, const Arr& DS
     // whose operand blocks are prefetched (cp.async, double buffered) while (k, s) runs.
     const char* const axp = AX.p;
     const char* const ayp = AY.p;
-    const uint32_t sb = AX.sb;
+    const uint32_t sbx = AX.sb, sby = AY.sb;  // arrays may hold different operand counts
     auto issue = [&](int kk, int ss, int buf) {
         const uint32_t b = sg.base + (uint32_t)(buf * 2 * (C / 4)) * sg.cs;
         const uint32_t cx = (uint32_t)ss * (C / 4), cy = (uint32_t)(kk - ss) * (C / 4);
 #pragma unroll
-        for (int q = 0; q < C / 4; q++) cp_async16(b + q * sg.cs, axp + (size_t)(cx + q) * sb);
+        for (int q = 0; q < C / 4; q++) cp_async16(b + q * sg.cs, axp + (size_t)(cx + q) * sbx);
         if (!(sqr && 2 * ss == kk)) {
 #pragma unroll
-            for (int q = 0; q < C / 4; q++) cp_async16(b + (C / 4 + q) * sg.cs, ayp + (size_t)(cy + q) * sb);
+            for (int q = 0; q < C / 4; q++) cp_async16(b + (C / 4 + q) * sg.cs, ayp + (size_t)(cy + q) * sby);
         }
         cp_commit();
     };

@@ -45,6 +45,8 @@ _SIGS = {
     "mont_batch_setup": (_i, [_vp, _vp, _vp, _sz, _i, _vp, _sz, _vp]),
     "mont_batch_setup_workspace": (_sz, [_sz, _i]),
     "mpb_modexp_host": (_i, [_vp, _vp, _vp, _vp, _sz, _i, _i, _i, _vp]),
+    "rsa_batch_crt_ct": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _i, _i, _i, _vp, _sz, _vp]),
+    "rsa_batch_crt_workspace": (_sz, [_sz, _i, _i]),
     "mpb_last_error": (ctypes.c_char_p, []),
 }
 for _name, (_res, _args) in _SIGS.items():
@@ -200,6 +202,21 @@ def mont_batch_modexp_ct(N, Np, R2, base, exp, bits: int, window: int = 5, redc:
     out = out if out is not None else empty_sliced(L, count, N.device)
     _check(_lib.mont_batch_modexp_ct(_ptr(N), _ptr(Np), _ptr(R2), _ptr(base), _ptr(exp), _ptr(out), count, bits,
                                      window, redc, algo, _ptr(ws), ws.numel() * 4, _stream()))
+    return out
+
+
+def rsa_workspace(count: int, bits: int, window: int, device="cuda") -> torch.Tensor:
+    return workspace(_lib.rsa_batch_crt_workspace(count, bits, window), device)
+
+
+def rsa_batch_crt_ct(c, p, q, dp, dq, qinv, bits: int, window: int = 5, redc: int = REDC_TRUNCATED,
+                     ws: torch.Tensor | None = None, out: torch.Tensor | None = None):
+    """m = c^d mod pq by CRT (word-sliced: c with L(bits) limbs, p/q/dp/dq/qinv with L(bits/2))."""
+    L, count = _sliced_shape(c)
+    ws = ws if ws is not None else rsa_workspace(count, bits, window, c.device)
+    out = out if out is not None else empty_sliced(L, count, c.device)
+    _check(_lib.rsa_batch_crt_ct(_ptr(c), _ptr(p), _ptr(q), _ptr(dp), _ptr(dq), _ptr(qinv), _ptr(out), count, bits,
+                                 window, redc, _ptr(ws), ws.numel() * 4, _stream()))
     return out
 
 

@@ -8,6 +8,7 @@ recompute one by one and check truncated == full REDC on the whole batch.
 """
 from __future__ import annotations
 
+import functools
 import random
 
 import numpy as np
@@ -285,3 +286,66 @@ def test_modexp_karatsuba_products(mpb, bits, algo):
     out = mpb.to_host(mpb.mont_batch_modexp_ct(dN, Np, R2, mpb.to_device(base), mpb.to_device(exp), bits,
                                                window=5, algo=algo))
     assert np.array_equal(out, O.batch_modexp(base, exp, bits, N))
+
+
+# ----------------------------------------------------------------- CRT-RSA (f4)
+@functools.lru_cache(maxsize=None)
+def _rsa_keys(bits: int, n_keys: int, seed: int):
+    """RSA keys from oracle primes (exactly bits/2 bits each), e = 65537."""
+    import math
+
+    h = bits // 2
+    keys = []
+    for i in range(n_keys):
+        while True:
+            p, q = O.gen_prime(h, seed + 2 * i), O.gen_prime(h, seed + 2 * i + 1 + 7919)
+            lam = (p - 1) * (q - 1) // math.gcd(p - 1, q - 1)
+            if p != q and math.gcd(65537, lam) == 1:
+                break
+            seed += 104729
+        d = O.inv_mod(65537, lam)
+        keys.append((p, q, d, d % (p - 1), d % (q - 1), O.inv_mod(q, p)))
+    return keys
+
+
+@pytest.mark.parametrize("redc", REDC)
+@pytest.mark.parametrize("bits", [512, 1024, 2048])
+def test_rsa_crt(mpb, bits, redc):
+    """Batched CRT-RSA private-key operation vs the oracle's CRT route and the full-size power
+    c^d mod n, with the edge ciphertexts 0, 1, n-1 and multiples of p and q; ragged count."""
+    n_keys, count = 5, 133
+    keys = _rsa_keys(bits, n_keys, seed=bits * 31 + 7)
+    L, Lh = I.limbs_for_bits(bits), I.limbs_for_bits(bits // 2)
+    rng = random.Random(bits + redc)
+    rows = []
+    for k in range(count):
+        p, q, d, dp, dq, qi = keys[k % n_keys]
+        n = p * q
+        c = [0, 1, n - 1, 3 * p, 5 * q][k] if k < 5 else rng.randrange(n)
+        rows.append((c, p, q, d, dp, dq, qi))
+    arrs = [I.ints_to_array([r[0] for r in rows], L)] + [I.ints_to_array([r[j] for r in rows], Lh) for j in (1, 2, 4, 5, 6)]
+    dc, dp_, dq_, ddp, ddq, dqi = (mpb.to_device(a) for a in arrs)
+    m = mpb.to_host(mpb.rsa_batch_crt_ct(dc, dp_, dq_, ddp, ddq, dqi, bits, window=5, redc=redc))
+    for k, (c, p, q, d, dp, dq, qi) in enumerate(rows):
+        got = I.from_limbs(m[k])
+        if k < 12:
+            assert got == O.rsa_crt(c, p, q, dp, dq, qi, Lh, bits // 2), k
+        assert got == pow(c, d, p * q), k
+
+
+def test_rsa_crt_round_trip(mpb):
+    """(msg^e)^d = msg for 2048-bit keys: the public operation by the oracle, the private one on the GPU."""
+    bits, count = 2048, 6
+    keys = _rsa_keys(bits, 3, seed=99)
+    L, Lh = I.limbs_for_bits(bits), I.limbs_for_bits(bits // 2)
+    rng = random.Random(4)
+    msgs, cts, ks = [], [], []
+    for k in range(count):
+        p, q, d, dp, dq, qi = keys[k % 3]
+        msg = rng.randrange(p * q)
+        msgs.append(msg)
+        cts.append(O.modexp(msg, 65537, p * q, L, ebits=17))
+        ks.append(keys[k % 3])
+    arrs = [I.ints_to_array(cts, L)] + [I.ints_to_array([kk[j] for kk in ks], Lh) for j in (0, 1, 3, 4, 5)]
+    m = mpb.to_host(mpb.rsa_batch_crt_ct(*(mpb.to_device(a) for a in arrs), bits))
+    assert [I.from_limbs(r) for r in m] == msgs

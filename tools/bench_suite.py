@@ -4,7 +4,7 @@ Prints one JSON object per measurement; each carries the algorithmic IMAD count,
 roofline fraction (148 SMs x 64 IMAD/clk x 1965 MHz = 18.61 T IMAD/s) and, where cheap,
 a parity verdict against the oracle on a seeded sample.
 
-  python tools/bench_suite.py [--configs 1,2,3,4,5] [--reps 3]
+  python tools/bench_suite.py [--configs 1,2,3,4,5,6] [--reps 3]     (6 = CRT-RSA)
 """
 from __future__ import annotations
 
@@ -156,6 +156,41 @@ def products(bits, count, reps):
                   "parity_sample": ok})
 
 
+def rsa_crt(bits, count, reps, n_keys=16):
+    """Batched CRT-RSA private-key operations: keys from oracle primes, a pool of
+    n_keys keys cycled over the batch (every item has its own ciphertext; the kernels' work per
+    item does not depend on which key it uses)."""
+    import math
+    import random
+
+    h = bits // 2
+    L, Lh = I.limbs_for_bits(bits), I.limbs_for_bits(h)
+    keys = []
+    for i in range(n_keys):
+        p, q = O.gen_prime(h, 1000 + 2 * i), O.gen_prime(h, 5000 + 2 * i)
+        lam = (p - 1) * (q - 1) // math.gcd(p - 1, q - 1)
+        d = O.inv_mod(65537, lam)
+        keys.append((p, q, d % (p - 1), d % (q - 1), O.inv_mod(q, p), d))
+    rng = random.Random(bits)
+    sel = [keys[k % n_keys] for k in range(count)]
+    cts = [rng.randrange(kk[0] * kk[1]) for kk in sel]
+    arrs = [I.ints_to_array(cts, L)] + [I.ints_to_array([kk[j] for kk in sel], Lh) for j in range(5)]
+    dev = [mpb.to_device(a) for a in arrs]
+    ws = mpb.rsa_workspace(count, bits, 5)
+    out = mpb.empty_sliced(L, count)
+    for redc, name in ((1, "truncated"), (0, "full"), (2, "cios")):
+        ms = timeit(lambda: mpb.rsa_batch_crt_ct(*dev, bits, 5, redc, ws=ws, out=out), reps, 1)
+        h_out = mpb.to_host(out)
+        idx = sample_idx(count, 8)
+        ok = all(I.from_limbs(h_out[k]) == pow(cts[k], sel[k][5], sel[k][0] * sel[k][1]) for k in idx)
+        imad = 2 * modexp_imad(h, 5, redc) * count
+        emit({"config": "crt-rsa", "op": "rsa_private_crt", "bits": bits, "count": count, "window": 5, "redc": name,
+              "ms": ms, "ops_per_s": count / (ms / 1e3), "imad_frac_modexp_basis": imad / (ms / 1e3) / PEAK,
+              "keys_in_pool": n_keys, "parity_sample_vs_pow": ok, "sample": len(idx)})
+    del dev, ws, out
+    torch.cuda.empty_cache()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="1,2,3,4,5")
@@ -178,6 +213,9 @@ def main():
         products(4154, 1 << 16, args.reps)
     if 5 in cfgs:
         modexp_run(5, 2048, 1 << 22, 1, redcs=((1, "truncated"),), check=64)
+    if 6 in cfgs:  # CRT-RSA (not a BASELINE config: SURVEY 8(f) f4)
+        rsa_crt(2048, 1 << 17, args.reps)
+        rsa_crt(4096, 1 << 14, args.reps)
 
 
 if __name__ == "__main__":
