@@ -121,20 +121,32 @@ MPB_DEVI void emit_block(const uint32_t (&W)[2 * C + 1], int j, int NB, bool add
 }
 
 // OUT = (ctop || !borrow) ? D : C, with D in OUT and C in T[NB..2NB) -- a mask, no branch.
+// Two blocks per step so that 4*(C/4) loads are in flight (the data was just written: L2 latency).
 template <int C>
 MPB_DEVI void final_select(int NB, const Arr& T, const Arr& OUT, uint32_t ctop, uint32_t borrow) {
     const uint32_t m = 0u - ((ctop | (borrow ^ 1u)) & 1u);  // all ones: take D = C - N
+    constexpr int Q = C / 4;
 #pragma unroll 1
-    for (int j = 0; j < NB; j++) {
+    for (int j = 0; j < NB; j += 2) {
+        uint4 d[2 * Q], c[2 * Q];
+        const bool two = j + 1 < NB;
 #pragma unroll
-        for (int q = 0; q < C / 4; q++) {
-            uint4 d = OUT.ld(j * (C / 4) + q);
-            const uint4 c = T.ld((NB + j) * (C / 4) + q);
-            d.x = (d.x & m) | (c.x & ~m);
-            d.y = (d.y & m) | (c.y & ~m);
-            d.z = (d.z & m) | (c.z & ~m);
-            d.w = (d.w & m) | (c.w & ~m);
-            OUT.st(j * (C / 4) + q, d);
+        for (int q = 0; q < 2 * Q; q++) {
+            if (q < Q || two) {
+                d[q] = OUT.ld(j * Q + q);
+                c[q] = T.ld((NB + j) * Q + q);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < 2 * Q; q++) {
+            if (q < Q || two) {
+                uint4 r;
+                r.x = (d[q].x & m) | (c[q].x & ~m);
+                r.y = (d[q].y & m) | (c[q].y & ~m);
+                r.z = (d[q].z & m) | (c[q].z & ~m);
+                r.w = (d[q].w & m) | (c[q].w & ~m);
+                OUT.st(j * Q + q, r);
+            }
         }
     }
 }
@@ -172,11 +184,21 @@ MPB_DEVI void engine(int ph, int NB, const Arr& AX, const Arr& AY, const Arr& DS
             carry = (orlo | tl1) != 0u ? 1u : 0u;  // c_add = [T mod R != 0]
             // corners: block column NB-2 contributes hi(q_s[C-1] * N_t[C-1]) at position L-1
 #pragma unroll 1
-            for (int s = 0; s + 2 <= NB; s++) {
-                const uint4 qv = AX.ld(s * (C / 4) + C / 4 - 1);
-                const uint4 nv = AY.ld((NB - 2 - s) * (C / 4) + C / 4 - 1);
-                asm volatile("mad.hi.cc.u32 %0, %2, %3, %0;\n\taddc.u32 %1, %1, 0;"
-                             : "+r"(W[0]), "+r"(W[1]) : "r"(qv.w), "r"(nv.w));
+            for (int s0 = 0; s0 + 2 <= NB; s0 += 4) {  // 4 corners per step: loads in flight together
+                uint32_t qw[4], nw[4];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    const int s = s0 + u;
+                    qw[u] = nw[u] = 0;
+                    if (s + 2 <= NB) {
+                        qw[u] = AX.ld(s * (C / 4) + C / 4 - 1).w;
+                        nw[u] = AY.ld((NB - 2 - s) * (C / 4) + C / 4 - 1).w;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; u++)
+                    asm volatile("mad.hi.cc.u32 %0, %2, %3, %0;\n\taddc.u32 %1, %1, 0;"
+                                 : "+r"(W[0]), "+r"(W[1]) : "r"(qw[u]), "r"(nw[u]));
             }
             orlo = 0u - tl1 - b;  // reuse: K = (-T[L-1] - b) mod 2^32
         }
