@@ -28,7 +28,11 @@ int fail(int code, const std::string& msg) {
     return code;
 }
 
+#ifdef MPB_THREADS
+constexpr int kThreads = MPB_THREADS;
+#else
 constexpr int kThreads = 128;
+#endif
 
 MPB_DEVI size_t tid_global() { return (size_t)blockIdx.x * blockDim.x + threadIdx.x; }
 

@@ -15,7 +15,11 @@
 
 namespace mpb {
 
+#ifdef MPB_THREADS
+constexpr int kThreads = MPB_THREADS;
+#else
 constexpr int kThreads = 128;
+#endif
 
 // resident CTAs per SM the heavy kernels are compiled for (register budget 65536 / (128 * minb))
 template <int C>

@@ -239,6 +239,86 @@ def test_config3_full_batch_sampled(mpb):
     assert np.array_equal(h[idx], ref)
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("bits", [1024, 2048, 3072, 4096])
+def test_config2_full_batch_sampled(mpb, bits):
+    """Config 2 at its full size (2^20 per size): MontMul and MontSqr, the three REDC modes equal
+    on the whole batch, a seeded sample against the oracle."""
+    count = 1 << 20
+    N, a, b = I.montmul_inputs(config=2, count=count, bits=bits)
+    dN, da, db = (mpb.to_device(x) for x in (N, a, b))
+    Np, _ = mpb.mont_batch_setup(dN, bits)
+    ws = mpb.mont_workspace(count, bits)
+    idx = np.concatenate([np.random.default_rng(bits).choice(count, size=12, replace=False), [0, count - 1]])
+    for op in ("mul", "sqr"):
+        outs = []
+        for redc in REDC:
+            if op == "mul":
+                outs.append(mpb.mont_batch_mul(da, db, dN, Np, bits, redc=redc, ws=ws))
+            else:
+                outs.append(mpb.mont_batch_sqr(da, dN, Np, bits, redc=redc, ws=ws))
+        assert all(torch.equal(outs[0], o) for o in outs[1:]), op
+        h = mpb.to_host(outs[0])
+        ref = O.batch_montmul(a[idx], (b if op == "mul" else a)[idx], N[idx])
+        assert np.array_equal(h[idx], ref), op
+
+
+@pytest.mark.slow
+def test_config4_full_batch_sampled(mpb):
+    """Config 4 at its full size (2^16): 4096-bit modexp with truncated / full / CIOS REDC and with
+    2-level Karatsuba products all equal on the whole batch; 4108 bits (L = 132, C = 12) sampled."""
+    count = 1 << 16
+    for bits, modes in ((4096, [(1, 1), (0, 1), (2, 1), (1, 3)]), (4108, [(1, 1)])):
+        N, base, exp = I.modexp_inputs(config=4, count=count, bits=bits)
+        dN, dB, dE = (mpb.to_device(x) for x in (N, base, exp))
+        Np, R2 = mpb.mont_batch_setup(dN, bits)
+        outs = [mpb.mont_batch_modexp_ct(dN, Np, R2, dB, dE, bits, 5, redc=r, algo=alg) for r, alg in modes]
+        assert all(torch.equal(outs[0], o) for o in outs[1:]), bits
+        h = mpb.to_host(outs[0])
+        idx = np.concatenate([np.random.default_rng(bits).choice(count, size=4, replace=False), [0, count - 1]])
+        assert np.array_equal(h[idx], O.batch_modexp(base[idx], exp[idx], bits, N[idx])), bits
+        del dN, dB, dE, Np, R2, outs
+        torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+def test_config5_full_batch_sampled(mpb):
+    """Config 5 at its full size (2^22 2048-bit modexps): eight contiguous slices (the 8-GPU plan,
+    run here as logical shards on one device) reproduce the whole-batch result byte for byte, and
+    a random 4096-element subset matches the oracle (BASELINE config 5)."""
+    from paper_2410_18129_b200 import shard
+
+    bits, count = 2048, 1 << 22
+    N, base, exp = I.modexp_inputs(config=5, count=count, bits=bits)
+    whole = shard.modexp_devices(N, base, exp, bits, devices=[0])
+    sliced = shard.modexp_devices(N, base, exp, bits, devices=[0] * 8)
+    assert np.array_equal(whole, sliced)
+    idx = np.random.default_rng(5).choice(count, size=4096, replace=False)
+    assert np.array_equal(whole[idx], O.batch_modexp(base[idx], exp[idx], bits, N[idx]))
+
+
+@pytest.mark.parametrize("bits", [8192, 16384])
+def test_products_at_maximum_size(mpb, bits):
+    """The largest supported operands (L = 256 and 512 limbs): schoolbook products and
+    Montgomery multiplication / squaring in all REDC modes against the oracle."""
+    count = 33
+    a, b = I.mul_inputs(config=4, count=count, bits=bits)
+    da, db = mpb.to_device(a), mpb.to_device(b)
+    c = mpb.to_host(mpb.mp_batch_mul(da, db, bits, 1))
+    A, B = ints(a), ints(b)
+    for k in range(0, count, 4):
+        assert I.from_limbs(c[k]) == O.mul(A[k], B[k]), k
+    N, x, y = I.montmul_inputs(config=2, count=count, bits=bits)
+    dN, dx, dy = (mpb.to_device(v) for v in (N, x, y))
+    Np, _ = mpb.mont_batch_setup(dN, bits)
+    idx = list(range(0, count, 8))
+    ref_m = O.batch_montmul(x[idx], y[idx], N[idx])
+    ref_s = O.batch_montmul(x[idx], x[idx], N[idx])
+    for redc in REDC:
+        assert np.array_equal(mpb.to_host(mpb.mont_batch_mul(dx, dy, dN, Np, bits, redc=redc))[idx], ref_m), redc
+        assert np.array_equal(mpb.to_host(mpb.mont_batch_sqr(dx, dN, Np, bits, redc=redc))[idx], ref_s), redc
+
+
 # ------------------------------------------------------------- ABI errors
 def test_abi_errors_and_noop(mpb):
     bits = 1024
