@@ -21,6 +21,8 @@ constexpr int kThreads = MPB_THREADS;
 constexpr int kThreads = 128;
 #endif
 
+static_assert(kThreads == (int)kStageThreads, "the engine's stage stride assumes blockDim == kThreads");
+
 // resident CTAs per SM the heavy kernels are compiled for (register budget 65536 / (128 * minb))
 template <int C>
 __host__ __device__ constexpr int min_blocks() {

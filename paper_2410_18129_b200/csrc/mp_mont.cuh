@@ -34,10 +34,16 @@ namespace mpb {
 // Word-sliced global array: chunk q (4 limbs, 16 bytes) of this thread's number at p + q*sb
 // (sb = count * 16 bytes).  The chunk address is one IMAD.WIDE.U32 (32-bit q times 32-bit sb
 // plus the 64-bit base).
+// p + idx * sb as ONE mad.wide.u32 (32 x 32 -> 64 plus the 64-bit base)
+MPB_DEVI char* chunk_addr(const char* p, uint32_t idx, uint32_t sb) {
+    uint64_t a;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(a) : "r"(idx), "r"(sb), "l"(reinterpret_cast<uint64_t>(p)));
+    return reinterpret_cast<char*>(a);
+}
 struct Arr {
     char* p;
     uint32_t sb;
-    MPB_DEVI uint4* addr(int q) const { return reinterpret_cast<uint4*>(p + (size_t)(uint32_t)q * sb); }
+    MPB_DEVI uint4* addr(int q) const { return reinterpret_cast<uint4*>(chunk_addr(p, (uint32_t)q, sb)); }
     MPB_DEVI uint4 ld(int q) const { return *addr(q); }
     MPB_DEVI uint4 ld_stream(int q) const { return __ldcs(addr(q)); }  // evict-first (table scans)
     MPB_DEVI void st(int q, uint4 v) const { *addr(q) = v; }
@@ -51,6 +57,14 @@ struct Stage {
     uint32_t base;
     uint32_t cs;
 };
+// Threads per CTA of every engine kernel (kernels.cuh kThreads): the stage stride blockDim * 16
+// is then a compile-time constant and every staging address is base + immediate.
+#ifdef MPB_THREADS
+constexpr uint32_t kStageThreads = MPB_THREADS;
+#else
+constexpr uint32_t kStageThreads = 128;
+#endif
+constexpr uint32_t kStageCS = kStageThreads * 16;
 MPB_DEVI void cp_async16(uint32_t saddr, const void* g) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
 }
@@ -210,13 +224,13 @@ MPB_DEVI void engine(int ph, int NB, const Arr& AX, const Arr& AY, const Arr& DS
     const char* const ayp = AY.p;
     const uint32_t sbx = AX.sb, sby = AY.sb;  // arrays may hold different operand counts
     auto issue = [&](int kk, int ss, int buf) {
-        const uint32_t b = sg.base + (uint32_t)(buf * 2 * (C / 4)) * sg.cs;
+        const uint32_t b = sg.base + (uint32_t)(buf * 2 * (C / 4)) * kStageCS;
         const uint32_t cx = (uint32_t)ss * (C / 4), cy = (uint32_t)(kk - ss) * (C / 4);
 #pragma unroll
-        for (int q = 0; q < C / 4; q++) cp_async16(b + q * sg.cs, axp + (size_t)(cx + q) * sbx);
+        for (int q = 0; q < C / 4; q++) cp_async16(b + q * kStageCS, chunk_addr(axp, cx + q, sbx));
         if (!(sqr && 2 * ss == kk)) {
 #pragma unroll
-            for (int q = 0; q < C / 4; q++) cp_async16(b + (C / 4 + q) * sg.cs, ayp + (size_t)(cy + q) * sby);
+            for (int q = 0; q < C / 4; q++) cp_async16(b + (C / 4 + q) * kStageCS, chunk_addr(ayp, cy + q, sby));
         }
         cp_commit();
     };
@@ -244,16 +258,16 @@ MPB_DEVI void engine(int ph, int NB, const Arr& AX, const Arr& AY, const Arr& DS
         const bool diag = sqr && s == t;
         uint32_t x[C], y[C];
         {
-            const uint32_t b = sg.base + (uint32_t)(buf * 2 * (C / 4)) * sg.cs;
+            const uint32_t b = sg.base + (uint32_t)(buf * 2 * (C / 4)) * kStageCS;
 #pragma unroll
             for (int q = 0; q < C / 4; q++) {
-                const uint4 v = lds128(b + q * sg.cs);
+                const uint4 v = lds128(b + q * kStageCS);
                 x[4 * q] = v.x; x[4 * q + 1] = v.y; x[4 * q + 2] = v.z; x[4 * q + 3] = v.w;
             }
             if (!diag) {
 #pragma unroll
                 for (int q = 0; q < C / 4; q++) {
-                    const uint4 v = lds128(b + (C / 4 + q) * sg.cs);
+                    const uint4 v = lds128(b + (C / 4 + q) * kStageCS);
                     y[4 * q] = v.x; y[4 * q + 1] = v.y; y[4 * q + 2] = v.z; y[4 * q + 3] = v.w;
                 }
             }
