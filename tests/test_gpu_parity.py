@@ -429,3 +429,45 @@ def test_rsa_crt_round_trip(mpb):
     arrs = [I.ints_to_array(cts, L)] + [I.ints_to_array([kk[j] for kk in ks], Lh) for j in (0, 1, 3, 4, 5)]
     m = mpb.to_host(mpb.rsa_batch_crt_ct(*(mpb.to_device(a) for a in arrs), bits))
     assert [I.from_limbs(r) for r in m] == msgs
+
+
+# ------------------------------------------------------------------ edge cases
+def test_empty_and_single_operand_batches(mpb):
+    """count = 0 is a no-op on every entry point; count = 1 is exact."""
+    bits = 1024
+    L = I.limbs_for_bits(bits)
+    z = mpb.empty_sliced(L, 0)
+    assert mpb.mont_batch_mul(z, z, z, z, bits).shape == (L // 4, 0, 4)
+    assert mpb.mont_batch_sqr(z, z, z, bits).shape == (L // 4, 0, 4)
+    assert mpb.mont_batch_modexp_ct(z, z, z, z, z, bits).shape == (L // 4, 0, 4)
+    zh = mpb.empty_sliced(L // 2, 0)
+    assert mpb.rsa_batch_crt_ct(z, zh, zh, zh, zh, zh, bits).shape == (L // 4, 0, 4)
+    N, base, exp = I.modexp_inputs(config=3, count=1, bits=bits)
+    dN = mpb.to_device(N)
+    Np, R2 = mpb.mont_batch_setup(dN, bits)
+    for redc in REDC:
+        out = mpb.to_host(mpb.mont_batch_modexp_ct(dN, Np, R2, mpb.to_device(base), mpb.to_device(exp), bits,
+                                                   redc=redc))
+        assert np.array_equal(out, O.batch_modexp(base, exp, bits, N)), redc
+
+
+@pytest.mark.parametrize("redc", REDC)
+def test_tiny_moduli(mpb, redc):
+    """Degenerate small moduli at the smallest width (bits = 32, L = 4, C = 4): N = 3, 5, 7, 2^31+1,
+    2^32-1 with every base below N (or a spread of them) and assorted exponents."""
+    bits = 32
+    L = I.limbs_for_bits(bits)
+    rows = []
+    for n in (3, 5, 7, (1 << 31) + 1, (1 << 32) - 1):
+        for b in ([0, 1, 2] if n <= 7 else [0, 1, 2, n - 1, n // 3]):
+            for e in (0, 1, 2, 3, (1 << 32) - 1, 0x80000001):
+                rows.append((n, b % n, e))
+    N = I.ints_to_array([r[0] for r in rows], L)
+    B = I.ints_to_array([r[1] for r in rows], L)
+    E = I.ints_to_array([r[2] for r in rows], L)
+    dN = mpb.to_device(N)
+    Np, R2 = mpb.mont_batch_setup(dN, bits)
+    out = mpb.to_host(mpb.mont_batch_modexp_ct(dN, Np, R2, mpb.to_device(B), mpb.to_device(E), bits, window=3,
+                                               redc=redc))
+    for k, (n, b, e) in enumerate(rows):
+        assert I.from_limbs(out[k]) == O.modexp(b, e, n, L, ebits=bits), (n, b, e)
