@@ -1,4 +1,5 @@
-"""One small call of every kernel family (for compute-sanitizer): layout, products (3 algorithms),
+"""One small call of every kernel family (a smoke of all launch paths; compute-sanitizer is closed on
+the GPU pool): layout, products (3 algorithms),
 Montgomery ops (3 REDC modes), REDC, setup, modexp (3 REDC modes, Karatsuba), CRT-RSA."""
 import os
 import sys
