@@ -10,6 +10,7 @@
 
 #include "launch.h"
 #include "mp_kara.cuh"
+#include "mp_coop.cuh"
 #include "mp_mont.cuh"
 #include "mp_setup.cuh"
 
@@ -119,13 +120,12 @@ __global__ void __launch_bounds__(kThreads) k_mont_redc(const uint32_t* __restri
 //   last op          out = REDC(Y)
 // workspace per operand (word-sliced, stride count): G (2^w * L) | Y (L) | T (2L) | Q (L) | S (L)
 //   | Karatsuba scratch (kara_scratch_blocks(nb, KLEV) blocks; KLEV = algo levels for the products)
-template <int C, int RM, int NBT, int KLEV>
-__global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_modexp(
-    const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP, const uint32_t* __restrict__ R2,
-    const uint32_t* __restrict__ base, const uint32_t* __restrict__ exp, uint32_t* __restrict__ out, size_t count,
-    int nb_rt, int bits, int w, uint32_t* ws) {
-    const size_t k = tid_global();
-    if (k >= count) return;
+// The whole exponentiation of operand k (of `count`, the arrays' stride).  COOP: two lanes per
+// operand (mp_coop.cuh), role = lane & 1, mask = the active pairs of the warp.
+template <int C, int RM, int NBT, int KLEV, bool COOP>
+MPB_DEVI void modexp_body(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
+                          const uint32_t* exp, uint32_t* out, size_t count, size_t k, int nb_rt, int bits, int w,
+                          uint32_t* ws, uint32_t role, unsigned mask) {
     const int nb = NBT ? NBT : nb_rt;  // compile-time block count for the hot sizes
     const int L = C * nb, Q4 = L / 4;
     const int nent = 1 << w;
@@ -180,7 +180,12 @@ __global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_modexp(
             const int pos = win * w, wi = pos >> 5, off = pos & 31;
             uint32_t v = word_at(exp, count, k, wi) >> off;
             if (off + w > 32 && wi + 1 < L) v |= word_at(exp, count, k, wi + 1) << (32 - off);
-            ct_select<select_unroll<C>()>(G, L, nent, v & ((1u << w) - 1u), O);
+            if constexpr (COOP) {  // the two lanes scan alternate chunk groups of every entry
+                ct_select<select_unroll<C>()>(G, L, nent, v & ((1u << w) - 1u), O, (int)role, 2);
+                __syncwarp(mask);
+            } else {
+                ct_select<select_unroll<C>()>(G, L, nent, v & ((1u << w) - 1u), O);
+            }
             continue;
         }
         if (RM != 2 && mode == MODE_REDC) {  // T = X zero-extended to 2L limbs (CIOS: MontMul(X, 1))
@@ -189,9 +194,44 @@ __global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_modexp(
                 T.st(q, X.ld(q));
                 T.st(Q4 + q, make_uint4(0, 0, 0, 0));
             }
+            if constexpr (COOP) __syncwarp(mask);
         }
-        mont_op_rm<C, RM, KLEV>(mode, nb, X, B, Nn, NPn, T, Q, O, KS, sg);
+        if constexpr (COOP) {
+            static_assert(RM != 2 && KLEV == 0, "cooperative operands: truncated or full REDC, schoolbook");
+            mont_op_coop<C, RM == 1>(mode, nb, X, B, Nn, NPn, T, Q, O, sg, role, mask);
+        } else {
+            mont_op_rm<C, RM, KLEV>(mode, nb, X, B, Nn, NPn, T, Q, O, KS, sg);
+        }
     }
+}
+
+// One thread per operand: operands k_ofs .. k_ofs + n_run - 1 of a batch of `count`.
+template <int C, int RM, int NBT, int KLEV>
+__global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_modexp(
+    const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP, const uint32_t* __restrict__ R2,
+    const uint32_t* __restrict__ base, const uint32_t* __restrict__ exp, uint32_t* __restrict__ out, size_t count,
+    size_t k_ofs, size_t n_run, int nb_rt, int bits, int w, uint32_t* ws) {
+    const size_t t = tid_global();
+    if (t >= n_run) return;
+    modexp_body<C, RM, NBT, KLEV, false>(N, NP, R2, base, exp, out, count, k_ofs + t, nb_rt, bits, w, ws, 0u,
+                                         0xFFFFFFFFu);
+}
+
+// Two lanes per operand (mp_coop.cuh): for batches below half the resident capacity and for the
+// partial last wave of larger ones.
+template <int C, int RM, int NBT>
+__global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_modexp_coop(
+    const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP, const uint32_t* __restrict__ R2,
+    const uint32_t* __restrict__ base, const uint32_t* __restrict__ exp, uint32_t* __restrict__ out, size_t count,
+    size_t k_ofs, size_t n_run, int nb_rt, int bits, int w, uint32_t* ws) {
+    const size_t t = tid_global();
+    if ((t >> 1) >= n_run) return;
+    // lanes of this warp that own an operand: pairs are never split (2 * n_run is even)
+    const size_t wbase = t & ~(size_t)31;
+    const size_t lanes = 2 * n_run - wbase;
+    const unsigned mask = lanes >= 32 ? 0xFFFFFFFFu : ((1u << lanes) - 1u);
+    modexp_body<C, RM, NBT, 0, true>(N, NP, R2, base, exp, out, count, k_ofs + (t >> 1), nb_rt, bits, w, ws,
+                                     (uint32_t)(t & 1), mask);
 }
 
 // ------------------------------------------------------------------- setup
@@ -425,33 +465,109 @@ void Launch<C>::mont_redc(const uint32_t* T, const uint32_t* N, const uint32_t* 
     if (trunc) k_mont_redc<C, true><<<grid_for(count), kThreads, sm, s>>>(T, N, NP, c, count, nb, ws);
     else k_mont_redc<C, false><<<grid_for(count), kThreads, sm, s>>>(T, N, NP, c, count, nb, ws);
 }
+// Split of a batch between the one-thread kernel (whole waves) and the cooperative kernel
+// (small batches, partial last wave); MPB_COOP=0 / 1 forces never / always (tuning and tests).
+// A per-thread, per-device auxiliary stream and fork/join events (created once, never destroyed).
+inline bool aux_stream(cudaStream_t* s2, cudaEvent_t* fork, cudaEvent_t* join) {
+    struct Aux {
+        int dev = -1;
+        cudaStream_t s = nullptr;
+        cudaEvent_t f = nullptr, j = nullptr;
+    };
+    thread_local Aux aux[16];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return false;
+    Aux& a = aux[dev];
+    if (a.dev != dev) {
+        if (cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking) != cudaSuccess) return false;
+        if (cudaEventCreateWithFlags(&a.f, cudaEventDisableTiming) != cudaSuccess) return false;
+        if (cudaEventCreateWithFlags(&a.j, cudaEventDisableTiming) != cudaSuccess) return false;
+        a.dev = dev;
+    }
+    *s2 = a.s;
+    *fork = a.f;
+    *join = a.j;
+    return true;
+}
+inline int coop_policy() {
+    static int v = [] {
+        const char* e = getenv("MPB_COOP");
+        return e ? atoi(e) : -1;
+    }();
+    return v;
+}
 template <int C>
 void Launch<C>::modexp(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
                        const uint32_t* exp, uint32_t* out, size_t count, int nb, int bits, int window, int redc,
                        int levels, uint32_t* ws, cudaStream_t s) {
     const size_t sm = stage_bytes<C>();
-    const unsigned g = grid_for(count);
     with_nb<C>(nb, [&](auto NBc) {
         constexpr int NBT = decltype(NBc)::value;
-        if (redc == 2) {  // CIOS: schoolbook rows only
-            k_modexp<C, 2, NBT, 0><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, nb, bits, window, ws);
-            return;
-        }
-        auto go = [&](auto KL) {
-            constexpr int KLEV = decltype(KL)::value;
-            if (redc == 1)
-                k_modexp<C, 1, NBT, KLEV><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, nb, bits, window,
-                                                                 ws);
-            else
-                k_modexp<C, 0, NBT, KLEV><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, nb, bits, window,
-                                                                 ws);
+        auto single = [&](size_t k0, size_t n) {
+            if (n == 0) return;
+            const unsigned g = grid_for(n);
+            if (redc == 2) {  // CIOS: schoolbook rows only
+                k_modexp<C, 2, NBT, 0><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, k0, n, nb, bits,
+                                                              window, ws);
+                return;
+            }
+            auto go = [&](auto KL) {
+                constexpr int KLEV = decltype(KL)::value;
+                if (redc == 1)
+                    k_modexp<C, 1, NBT, KLEV><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, k0, n, nb,
+                                                                     bits, window, ws);
+                else
+                    k_modexp<C, 0, NBT, KLEV><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, k0, n, nb,
+                                                                     bits, window, ws);
+            };
+            // Karatsuba product phases are compiled for the large shapes only (f1); elsewhere schoolbook
+            if constexpr (NBT == 0 || NBT == 8 || NBT == 11) {
+                if (levels >= 2) return go(std::integral_constant<int, 2>{});
+                if (levels == 1) return go(std::integral_constant<int, 1>{});
+            }
+            go(std::integral_constant<int, 0>{});
         };
-        // Karatsuba product phases are compiled for the large shapes only (f1); elsewhere schoolbook
-        if constexpr (NBT == 0 || NBT == 8 || NBT == 11) {
-            if (levels >= 2) return go(std::integral_constant<int, 2>{});
-            if (levels == 1) return go(std::integral_constant<int, 1>{});
+        auto coop = [&](size_t k0, size_t n) {
+            if (n == 0) return;
+            const unsigned g = grid_for(2 * n);
+            if (redc == 1)
+                k_modexp_coop<C, 1, NBT><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, k0, n, nb, bits,
+                                                                window, ws);
+            else
+                k_modexp_coop<C, 0, NBT><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, k0, n, nb, bits,
+                                                                window, ws);
+        };
+        const int pol = coop_policy();
+        if (redc == 2 || levels > 0 || pol == 0) return single(0, count);
+        if (pol == 1) return coop(0, count);
+        // Measured: two lanes per operand pay for >= 3072-bit operands at low
+        // occupancy (1.23x at 4096 bits); at 1024/2048 bits or near half occupancy they do not.
+        if (C * nb < 96) return single(0, count);
+        int dev = 0, sms = 148, per_sm = min_blocks<C>();
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_modexp<C, 1, NBT, 0>, kThreads, sm);
+        const size_t slots = (size_t)sms * (size_t)(per_sm > 0 ? per_sm : 1) * kThreads;
+        if (4 * count <= slots) return coop(0, count);  // small batch
+        const size_t tail = count % slots;
+        if (count > slots && tail > 0 && 4 * tail <= slots) {
+            // whole waves on `s`; the cooperative tail on a second stream, launched after them so its
+            // CTAs take the slots the last wave frees (fork / join with events: still asynchronous)
+            cudaStream_t s2;
+            cudaEvent_t fork, join;
+            if (aux_stream(&s2, &fork, &join)) {
+                cudaEventRecord(fork, s);
+                cudaStreamWaitEvent(s2, fork, 0);
+                single(0, count - tail);
+                cudaStream_t keep = s;
+                s = s2;
+                coop(count - tail, tail);
+                s = keep;
+                cudaEventRecord(join, s2);
+                cudaStreamWaitEvent(s, join, 0);
+                return;
+            }
         }
-        go(std::integral_constant<int, 0>{});
+        single(0, count);
     });
 }
 

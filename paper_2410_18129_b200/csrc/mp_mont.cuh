@@ -112,7 +112,7 @@ MPB_DEVI void w_shift(uint32_t (&W)[2 * C + 1]) {  // W >>= 32C
 // of C itself (full); C is parked in T block NB+j and D = C - N - borrow goes to OUT block j.
 template <int C>
 MPB_DEVI void emit_block(const uint32_t (&W)[2 * C + 1], int j, int NB, bool add_thi, const Arr& T, const Arr& N,
-                         const Arr& OUT, uint32_t& carry, uint32_t& borrow) {
+                         const Arr& OUT, uint32_t& carry, uint32_t& borrow, bool wr = true) {
     uint32_t c[C];
 #pragma unroll
     for (int i = 0; i < C; i++) c[i] = W[i];
@@ -124,20 +124,20 @@ MPB_DEVI void emit_block(const uint32_t (&W)[2 * C + 1], int j, int NB, bool add
         for (int i = 0; i < C; i++) add_next(c[i], t[i]);
         carry = cc_save();
     }
-    stb<C>(T, NB + j, c);
+    if (wr) stb<C>(T, NB + j, c);
     uint32_t n[C];
     ldb<C>(N, j, n);
     bc_restore(borrow);
 #pragma unroll
     for (int i = 0; i < C; i++) sub_next(c[i], n[i]);
     borrow = bc_save();
-    stb<C>(OUT, j, c);
+    if (wr) stb<C>(OUT, j, c);
 }
 
 // OUT = (ctop || !borrow) ? D : C, with D in OUT and C in T[NB..2NB) -- a mask, no branch.
 // Two blocks per step so that 4*(C/4) loads are in flight (the data was just written: L2 latency).
 template <int C>
-MPB_DEVI void final_select(int NB, const Arr& T, const Arr& OUT, uint32_t ctop, uint32_t borrow) {
+MPB_DEVI void final_select(int NB, const Arr& T, const Arr& OUT, uint32_t ctop, uint32_t borrow, bool wr = true) {
     const uint32_t m = 0u - ((ctop | (borrow ^ 1u)) & 1u);  // all ones: take D = C - N
     constexpr int Q = C / 4;
 #pragma unroll 1
@@ -159,7 +159,7 @@ MPB_DEVI void final_select(int NB, const Arr& T, const Arr& OUT, uint32_t ctop, 
                 r.y = (d[q].y & m) | (c[q].y & ~m);
                 r.z = (d[q].z & m) | (c[q].z & ~m);
                 r.w = (d[q].w & m) | (c[q].w & ~m);
-                OUT.st(j * Q + q, r);
+                if (wr) OUT.st(j * Q + q, r);
             }
         }
     }
@@ -467,8 +467,10 @@ MPB_DEVI void cios_op(int NB, const Arr& X, const Arr& B, bool b_one, const Arr&
 // Entry e, chunk q lives at chunk index e*(L/4) + q of G.  The scan is bound by DRAM latency
 // (the tables of all resident operands exceed L2), so it keeps SEL_U entries x SEL_G chunks of
 // loads in flight per step; accumulators stay in registers at every L.
+// part / nparts: this thread scans chunk groups part, part + nparts, ... (cooperative operands
+// split the scan between their lanes; every entry is still read in full by the operand's lanes).
 template <int U>
-MPB_DEVI void ct_select(const Arr& G, int L, int nent, uint32_t idx, const Arr& OUT) {
+MPB_DEVI void ct_select(const Arr& G, int L, int nent, uint32_t idx, const Arr& OUT, int part = 0, int nparts = 1) {
     const int Q4 = L / 4;
 
 #ifdef MPB_SEL_G
@@ -477,7 +479,7 @@ MPB_DEVI void ct_select(const Arr& G, int L, int nent, uint32_t idx, const Arr& 
     constexpr int GRP = 4;
 #endif
 #pragma unroll 1
-    for (int g0 = 0; g0 < Q4; g0 += GRP) {
+    for (int g0 = part * GRP; g0 < Q4; g0 += nparts * GRP) {
         uint4 acc[GRP];
 #pragma unroll
         for (int q = 0; q < GRP; q++) acc[q] = make_uint4(0, 0, 0, 0);

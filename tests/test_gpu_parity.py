@@ -471,3 +471,44 @@ def test_tiny_moduli(mpb, redc):
                                                redc=redc))
     for k, (n, b, e) in enumerate(rows):
         assert I.from_limbs(out[k]) == O.modexp(b, e, n, L, ebits=bits), (n, b, e)
+
+
+# ------------------------------------------------ one-thread vs two-lane operands
+_COOP_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+from paper_2410_18129_b200 import inputs as I, mpb
+out = {}
+for bits, count, w, redc in ((1024, 9, 5, 1), (2048, 5, 4, 0), (3072, 4, 5, 1), (4096, 3, 5, 0), (4108, 2, 3, 1)):
+    N, base, exp = I.modexp_inputs(config=4, count=count, bits=bits)
+    dN = mpb.to_device(N)
+    Np, R2 = mpb.mont_batch_setup(dN, bits)
+    o = mpb.to_host(mpb.mont_batch_modexp_ct(dN, Np, R2, mpb.to_device(base), mpb.to_device(exp), bits, window=w,
+                                             redc=redc))
+    print(bits, count, w, redc, o.tobytes().hex())
+"""
+
+
+@pytest.mark.parametrize("coop", ["0", "1"])
+def test_modexp_one_thread_and_two_lane_kernels(mpb, coop):
+    """Both exponentiation kernels, forced by MPB_COOP in a subprocess (the policy is read once per
+    process): one thread per operand (0) and two lanes per operand (1, mp_coop.cuh), 1024..4108 bits,
+    truncated and full REDC, against the oracle."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MPB_COOP=coop)
+    res = subprocess.run([sys.executable, "-c", _COOP_SCRIPT % root], env=env, capture_output=True, text=True,
+                         timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [l for l in res.stdout.splitlines() if l.strip()]
+    assert len(lines) == 5
+    for line in lines:
+        bits, count, w, redc, hx = line.split()
+        bits, count = int(bits), int(count)
+        L = I.limbs_for_bits(bits)
+        got = np.frombuffer(bytes.fromhex(hx), dtype=np.uint32).reshape(count, L)
+        N, base, exp = I.modexp_inputs(config=4, count=count, bits=bits)
+        assert np.array_equal(got, O.batch_modexp(base, exp, bits, N)), (bits, coop)
