@@ -30,7 +30,7 @@
  *
  * Errors.  MPB_EINVAL: null / misaligned / aliasing pointer, redc or algo out of range,
  * window not in 1..6, workspace too small (SPEC "shape"/"usage" errors).  MPB_EUNSUPPORTED:
- * bits out of range (SPEC "configuration error").  MPB_ECUDA: launch failure; text via mpb_last_error().
+ * bits out of range, count > 2^27 operands per call (SPEC "configuration error").  MPB_ECUDA: launch failure; text via mpb_last_error().
  */
 #ifndef PAPER_2410_18129_MPB_H
 #define PAPER_2410_18129_MPB_H

@@ -97,6 +97,9 @@ int check_launch() {
 unsigned grid_for(size_t n) { return (unsigned)((n + kThreads - 1) / kThreads); }
 
 constexpr int kMaxLimbs = 512;  // 16384-bit operands
+// Word-sliced chunk strides are count * 16 bytes held in 32 bits (one mad.wide.u32 per address);
+// the CRT path holds 2 * count operands.
+constexpr size_t kMaxCount = (size_t)1 << 27;
 
 int limbs_checked(int bits, int& L) {
     L = mpb_limbs(bits);
@@ -127,6 +130,7 @@ const char* mpb_last_error(void) { return g_err.c_str(); }
 int mpb_layout_expand(const uint32_t* src, uint32_t* dst, size_t count, int limbs, void* stream) {
     g_err.clear();
     if (count == 0) return MPB_OK;
+    if (count > kMaxCount) return fail(MPB_EUNSUPPORTED, "count exceeds 2^27 operands per call");
     if (limbs <= 0 || limbs % 4) return fail(MPB_EINVAL, "limbs must be a positive multiple of 4");
     if (int rc = check_ptrs({src, dst})) return rc;
     if (src == dst) return fail(MPB_EINVAL, "in-place layout change not supported");
@@ -138,6 +142,7 @@ int mpb_layout_expand(const uint32_t* src, uint32_t* dst, size_t count, int limb
 int mpb_layout_contract(const uint32_t* src, uint32_t* dst, size_t count, int limbs, void* stream) {
     g_err.clear();
     if (count == 0) return MPB_OK;
+    if (count > kMaxCount) return fail(MPB_EUNSUPPORTED, "count exceeds 2^27 operands per call");
     if (limbs <= 0 || limbs % 4) return fail(MPB_EINVAL, "limbs must be a positive multiple of 4");
     if (int rc = check_ptrs({src, dst})) return rc;
     if (src == dst) return fail(MPB_EINVAL, "in-place layout change not supported");
@@ -171,6 +176,7 @@ static int mp_product(const uint32_t* a, const uint32_t* b, uint32_t* c, size_t 
     int L;
     if (int rc = limbs_checked(bits, L)) return rc;
     if (count == 0) return MPB_OK;
+    if (count > kMaxCount) return fail(MPB_EUNSUPPORTED, "count exceeds 2^27 operands per call");
     if (int rc = check_ptrs({a, b, c})) return rc;
     if (c == a || c == b) return fail(MPB_EINVAL, "output aliases an input");
     const int levels = kara_levels(algo, L);
@@ -209,6 +215,7 @@ static int mont_op(const uint32_t* a, const uint32_t* b, const uint32_t* N, cons
     int L;
     if (int rc = limbs_checked(bits, L)) return rc;
     if (count == 0) return MPB_OK;
+    if (count > kMaxCount) return fail(MPB_EUNSUPPORTED, "count exceeds 2^27 operands per call");
     if (int rc = check_ptrs({a, b, N, NP, c, ws})) return rc;
     if (c == a || c == b || c == N || c == NP) return fail(MPB_EINVAL, "output aliases an input");
     if (ws_bytes < mont_batch_workspace(count, bits)) return fail(MPB_EINVAL, "workspace too small");
@@ -238,6 +245,7 @@ int mont_batch_redc(const uint32_t* T, const uint32_t* N, const uint32_t* NP, ui
     int L;
     if (int rc = limbs_checked(bits, L)) return rc;
     if (count == 0) return MPB_OK;
+    if (count > kMaxCount) return fail(MPB_EUNSUPPORTED, "count exceeds 2^27 operands per call");
     if (int rc = check_ptrs({T, N, NP, c, ws})) return rc;
     if (c == T || c == N || c == NP) return fail(MPB_EINVAL, "output aliases an input");
     if (ws_bytes < mont_batch_workspace(count, bits)) return fail(MPB_EINVAL, "workspace too small");
@@ -269,6 +277,7 @@ int mont_batch_modexp_ct(const uint32_t* N, const uint32_t* NP, const uint32_t* 
     int L;
     if (int rc = limbs_checked(bits, L)) return rc;
     if (count == 0) return MPB_OK;
+    if (count > kMaxCount) return fail(MPB_EUNSUPPORTED, "count exceeds 2^27 operands per call");
     if (int rc = check_ptrs({N, NP, R2, base, exp, out, ws})) return rc;
     if (out == N || out == NP || out == R2 || out == base || out == exp)
         return fail(MPB_EINVAL, "output aliases an input");
@@ -293,6 +302,7 @@ int mont_batch_setup(const uint32_t* N, uint32_t* NP, uint32_t* R2, size_t count
     int L;
     if (int rc = limbs_checked(bits, L)) return rc;
     if (count == 0) return MPB_OK;
+    if (count > kMaxCount) return fail(MPB_EUNSUPPORTED, "count exceeds 2^27 operands per call");
     if (int rc = check_ptrs({N, NP, R2, ws})) return rc;
     if (NP == N || R2 == N || NP == R2) return fail(MPB_EINVAL, "output aliases an input");
     if (ws_bytes < mont_batch_setup_workspace(count, bits)) return fail(MPB_EINVAL, "workspace too small");
@@ -334,6 +344,7 @@ int rsa_batch_crt_ct(const uint32_t* c, const uint32_t* p, const uint32_t* q, co
     if (int rc = limbs_checked(bits, L)) return rc;
     if (int rc = limbs_checked(bits / 2, Lh)) return rc;
     if (count == 0) return MPB_OK;
+    if (count > kMaxCount) return fail(MPB_EUNSUPPORTED, "count exceeds 2^27 operands per call");
     if (int rc = check_ptrs({c, p, q, dp, dq, qinv, m, ws})) return rc;
     for (const void* in : {(const void*)c, (const void*)p, (const void*)q, (const void*)dp, (const void*)dq,
                            (const void*)qinv})
@@ -378,6 +389,7 @@ int mpb_modexp_host(const uint32_t* N, const uint32_t* base, const uint32_t* exp
     if (int rc = limbs_checked(bits, L)) return rc;
     if (!redc_ok(redc)) return fail(MPB_EINVAL, "redc out of range");
     if (count == 0) return MPB_OK;
+    if (count > kMaxCount) return fail(MPB_EUNSUPPORTED, "count exceeds 2^27 operands per call");
     if (!N || !base || !exp || !out) return fail(MPB_EINVAL, "null pointer");
     cudaStream_t s = (cudaStream_t)stream;
     const size_t nb = count * (size_t)L * sizeof(uint32_t);

@@ -87,3 +87,24 @@ def test_binding_fails_loudly_without_library(tmp_path, monkeypatch):
     mod = importlib.util.module_from_spec(spec)
     with pytest.raises(ImportError):
         spec.loader.exec_module(mod)
+
+
+def test_host_side_argument_checks(lib):
+    """Argument errors are reported before any device work (no GPU needed): count beyond 2^27,
+    bits beyond 16384, window / redc / algo out of range, null pointers; count 0 is a no-op."""
+    vp, sz, i = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
+    lib.mont_batch_mul.argtypes = [vp, vp, vp, vp, vp, sz, i, i, vp, sz, vp]
+    lib.mont_batch_modexp_ct.argtypes = [vp, vp, vp, vp, vp, vp, sz, i, i, i, i, vp, sz, vp]
+    lib.mpb_last_error.restype = ctypes.c_char_p
+    EINVAL, EUNSUPPORTED = -1, -2
+    big = (1 << 27) + 1
+    assert lib.mont_batch_mul(None, None, None, None, None, big, 1024, 1, None, 0, None) == EUNSUPPORTED
+    assert b"2^27" in lib.mpb_last_error()
+    assert lib.mont_batch_mul(None, None, None, None, None, 4, 20000, 1, None, 0, None) == EUNSUPPORTED
+    assert lib.mont_batch_mul(None, None, None, None, None, 4, 1024, 7, None, 0, None) == EINVAL
+    assert lib.mont_batch_mul(None, None, None, None, None, 4, 1024, 1, None, 0, None) == EINVAL  # null
+    assert lib.mont_batch_mul(None, None, None, None, None, 0, 1024, 1, None, 0, None) == 0  # no-op
+    assert lib.mont_batch_modexp_ct(None, None, None, None, None, None, 4, 1024, 7, 1, 0, None, 0, None) == EINVAL
+    assert lib.mont_batch_modexp_ct(None, None, None, None, None, None, 4, 1024, 5, 1, 9, None, 0, None) == EINVAL
+    assert lib.mont_batch_modexp_ct(None, None, None, None, None, None, big, 1024, 5, 1, 0, None, 0, None) \
+        == EUNSUPPORTED
