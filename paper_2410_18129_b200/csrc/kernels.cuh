@@ -2,6 +2,7 @@
 // Templated on the block size C only; the block count nb = L / C is a runtime argument.
 // Instantiated once per C in inst_C*.cu; api.cu holds the C ABI and sees only launch.h.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -42,9 +43,16 @@ __host__ __device__ constexpr int select_unroll() {
     return 4;
 #endif
 }
-// dynamic shared memory: 2 buffers x 2 operand blocks x C/4 chunks of 16 bytes per thread
+// dynamic shared memory: 2 buffers x 2 operand blocks x C/4 chunks of 16 bytes per thread (as
+// per-thread cp.async chunks or as per-warp TMA tiles), then two mbarriers per warp
 template <int C>
-constexpr size_t stage_bytes() { return (size_t)kThreads * 4 * (C / 4) * 16; }
+constexpr size_t stage_bytes() { return (size_t)kThreads * 4 * (C / 4) * 16 + (kThreads / 32) * 16; }
+
+// TMA tensor maps of the exponentiation's arrays (2-D: 4*count words x chunk rows)
+enum { TM_N = 1, TM_NP, TM_R2, TM_BASE, TM_G, TM_Y, TM_T, TM_Q, TM_S, TM_COUNT = 9 };
+struct TmaMaps {
+    CUtensorMap m[TM_COUNT];
+};
 
 MPB_DEVI size_t tid_global() { return (size_t)blockIdx.x * blockDim.x + threadIdx.x; }
 // word-sliced accessor for operand k of an array with `count` operands
@@ -53,8 +61,30 @@ MPB_DEVI Arr arr(const uint32_t* base, size_t count, size_t k) {
 }
 // this thread's staging area in dynamic shared memory
 MPB_DEVI Stage stage() {
-    extern __shared__ uint4 smem_stage[];
+    extern __shared__ __align__(128) uint4 smem_stage[];
     return Stage{(uint32_t)__cvta_generic_to_shared(smem_stage + threadIdx.x), (uint32_t)(blockDim.x * 16)};
+}
+// TMA staging: this warp's 2 x 2 tiles and its two mbarriers (initialised here); kw = the warp's
+// first operand.  Every lane of the warp calls this (lane 0 of the active ones initialises).
+template <int C>
+MPB_DEVI Stage stage_tma(size_t kw, const TmaMaps* maps) {
+    extern __shared__ __align__(128) uint4 smem_stage[];
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(smem_stage);
+    const uint32_t warp = threadIdx.x >> 5;
+    constexpr uint32_t tile = (C / 4) * 512u;
+    Stage sg{};
+    sg.tbase = base + warp * 4u * tile;
+    sg.tbar = base + (uint32_t)kThreads * 4u * (C / 4) * 16u + warp * 16u;
+    sg.kw = (uint32_t)kw;
+    sg.amask = __activemask();
+    sg.maps = maps;
+    if ((threadIdx.x & 31u) == 0) {
+        mbar_init(sg.tbar, 1);
+        mbar_init(sg.tbar + 8, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp(sg.amask);
+    return sg;
 }
 // word i of operand k (32-bit access)
 MPB_DEVI uint32_t word_at(const uint32_t* base, size_t count, size_t k, int i) {
@@ -122,10 +152,10 @@ __global__ void __launch_bounds__(kThreads) k_mont_redc(const uint32_t* __restri
 //   | Karatsuba scratch (kara_scratch_blocks(nb, KLEV) blocks; KLEV = algo levels for the products)
 // The whole exponentiation of operand k (of `count`, the arrays' stride).  COOP: two lanes per
 // operand (mp_coop.cuh), role = lane & 1, mask = the active pairs of the warp.
-template <int C, int RM, int NBT, int KLEV, bool COOP>
+template <int C, int RM, int NBT, int KLEV, bool COOP, bool TMA = false>
 MPB_DEVI void modexp_body(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
                           const uint32_t* exp, uint32_t* out, size_t count, size_t k, int nb_rt, int bits, int w,
-                          uint32_t* ws, uint32_t role, unsigned mask) {
+                          uint32_t* ws, uint32_t role, unsigned mask, const TmaMaps* maps = nullptr) {
     const int nb = NBT ? NBT : nb_rt;  // compile-time block count for the hot sizes
     const int L = C * nb, Q4 = L / 4;
     const int nent = 1 << w;
@@ -143,7 +173,14 @@ MPB_DEVI void modexp_body(const uint32_t* N, const uint32_t* NP, const uint32_t*
     const Arr KS = arr(p, count, k);  // Karatsuba scratch (KLEV > 0)
     const Arr Nn = arr(N, count, k), NPn = arr(NP, count, k), R2n = arr(R2, count, k), Bn = arr(base, count, k);
     const Arr On = arr(out, count, k);
-    const Stage sg = stage();
+    Stage sg = stage();
+    uint32_t tph = 0;  // TMA: mbarrier phase bits of the two tile buffers
+    Arr Gt = G, Yt = Y, Tt = T, Qt = Q, St = S, Nt = Nn, NPt = NPn, R2t = R2n, Bt = Bn;
+    if constexpr (TMA) {  // the same arrays, tagged with their tensor maps
+        sg = stage_tma<C>(k - (threadIdx.x & 31u), maps);
+        Gt.tm = TM_G; Yt.tm = TM_Y; Tt.tm = TM_T; Qt.tm = TM_Q; St.tm = TM_S;
+        Nt.tm = TM_N; NPt.tm = TM_NP; R2t.tm = TM_R2; Bt.tm = TM_BASE;
+    }
 
     const int nwin = (bits + w - 1) / w;
     const int per_win = w + 2;
@@ -153,26 +190,26 @@ MPB_DEVI void modexp_body(const uint32_t* N, const uint32_t* NP, const uint32_t*
         int mode = MODE_MUL;
         bool select = false;
         int win = 0;
-        Arr X = Y, B = Y, O = Y;
+        Arr X = Yt, B = Yt, O = Yt;
         if (op == 0) {
-            mode = MODE_REDC; X = R2n; O = G;
+            mode = MODE_REDC; X = R2t; O = Gt;
         } else if (op < nent) {
-            X = op == 1 ? Bn : G.at((op - 1) * Q4);
-            B = op == 1 ? R2n : G.at(Q4);
-            O = G.at(op * Q4);
+            X = op == 1 ? Bt : Gt.at((op - 1) * Q4);
+            B = op == 1 ? R2t : Gt.at(Q4);
+            O = Gt.at(op * Q4);
         } else if (op == nent) {
-            select = true; win = nwin - 1; O = Y;
+            select = true; win = nwin - 1; O = Yt;
         } else if (op == n_ops - 1) {
-            mode = MODE_REDC; X = Y; O = On;
+            mode = MODE_REDC; X = Yt; O = On;
         } else {
             const int r = (op - nent - 1) % per_win;
             win = nwin - 2 - (op - nent - 1) / per_win;
             if (r < w) {
                 mode = MODE_SQR;
             } else if (r == w) {
-                select = true; O = S;
+                select = true; O = St;
             } else {
-                B = S;
+                B = St;
             }
         }
         if (select) {
@@ -199,6 +236,9 @@ MPB_DEVI void modexp_body(const uint32_t* N, const uint32_t* NP, const uint32_t*
         if constexpr (COOP) {
             static_assert(RM != 2 && KLEV == 0, "cooperative operands: truncated or full REDC, schoolbook");
             mont_op_coop<C, RM == 1>(mode, nb, X, B, Nn, NPn, T, Q, O, sg, role, mask);
+        } else if constexpr (TMA) {
+            static_assert(RM != 2 && KLEV == 0, "TMA operand tiles: truncated or full REDC, schoolbook");
+            mont_op<C, RM == 1, true>(mode, nb, X, B, Nt, NPt, Tt, Qt, O, sg, &tph);
         } else {
             mont_op_rm<C, RM, KLEV>(mode, nb, X, B, Nn, NPn, T, Q, O, KS, sg);
         }
@@ -215,6 +255,18 @@ __global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_modexp(
     if (t >= n_run) return;
     modexp_body<C, RM, NBT, KLEV, false>(N, NP, R2, base, exp, out, count, k_ofs + t, nb_rt, bits, w, ws, 0u,
                                          0xFFFFFFFFu);
+}
+
+// One thread per operand, operand blocks loaded as per-warp TMA tiles (engine<.., TMA = true>).
+template <int C, int RM, int NBT>
+__global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_modexp_tma(
+    const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP, const uint32_t* __restrict__ R2,
+    const uint32_t* __restrict__ base, const uint32_t* __restrict__ exp, uint32_t* __restrict__ out, size_t count,
+    size_t k_ofs, size_t n_run, int nb_rt, int bits, int w, uint32_t* ws, const __grid_constant__ TmaMaps maps) {
+    const size_t t = tid_global();
+    if (t >= n_run) return;
+    modexp_body<C, RM, NBT, 0, false, true>(N, NP, R2, base, exp, out, count, k_ofs + t, nb_rt, bits, w, ws, 0u,
+                                            0xFFFFFFFFu, &maps);
 }
 
 // Two lanes per operand (mp_coop.cuh): for batches below half the resident capacity and for the
@@ -489,6 +541,38 @@ inline bool aux_stream(cudaStream_t* s2, cudaEvent_t* fork, cudaEvent_t* join) {
     *join = a.j;
     return true;
 }
+// TMA tensor map of a word-sliced array: 2-D, dim 0 = 4*count uint32 words (all operands' chunk
+// rows), dim 1 = rows (chunks per operand), row stride count*16 bytes; box = 128 words (one warp's
+// 32 operands) x box_rows (one block); out-of-range operands read as zero.
+inline bool encode_tile_map(CUtensorMap* m, const uint32_t* base, size_t count, int rows, int box_rows) {
+    using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                            const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                            CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Fn fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return (Fn) nullptr;
+        return (Fn)f;
+    }();
+    if (!fn) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)count * 4, (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)count * 16};
+    const cuuint32_t box[2] = {128, (cuuint32_t)box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, const_cast<uint32_t*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// MPB_TMA=1 selects the TMA operand tiles (tests and measurements)
+inline int tma_policy() {
+    static int v = [] {
+        const char* e = getenv("MPB_TMA");
+        return e ? atoi(e) : -1;
+    }();
+    return v;
+}
 inline int coop_policy() {
     static int v = [] {
         const char* e = getenv("MPB_COOP");
@@ -538,6 +622,31 @@ void Launch<C>::modexp(const uint32_t* N, const uint32_t* NP, const uint32_t* R2
                                                                 window, ws);
         };
         const int pol = coop_policy();
+        if (redc != 2 && levels == 0 && pol != 1 && tma_policy() == 1) {
+            // opt-in (MPB_TMA=1): one thread per operand with per-warp TMA operand tiles -- correct,
+            // but 10 % slower than the cp.async.ca stage, whose operand blocks re-hit in L1
+            // (DESIGN.md 5.3); falls back when the tensor maps cannot be encoded
+            TmaMaps maps;
+            const int L = C * nb;
+            const uint32_t* arrs[TM_COUNT] = {N, NP, R2, base, ws, ws + (size_t)(1 << window) * L * count,
+                                              ws + (size_t)((1 << window) + 1) * L * count,
+                                              ws + (size_t)((1 << window) + 3) * L * count,
+                                              ws + (size_t)((1 << window) + 4) * L * count};
+            const int rows[TM_COUNT] = {L / 4, L / 4, L / 4, L / 4, (1 << window) * L / 4, L / 4, 2 * L / 4, L / 4,
+                                        L / 4};
+            bool ok = true;
+            for (int i = 0; i < TM_COUNT && ok; i++) ok = encode_tile_map(&maps.m[i], arrs[i], count, rows[i], C / 4);
+            if (ok) {
+                const unsigned g = grid_for(count);
+                if (redc == 1)
+                    k_modexp_tma<C, 1, NBT><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, 0, count, nb,
+                                                                   bits, window, ws, maps);
+                else
+                    k_modexp_tma<C, 0, NBT><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, 0, count, nb,
+                                                                   bits, window, ws, maps);
+                return;
+            }
+        }
         if (redc == 2 || levels > 0 || pol == 0) return single(0, count);
         if (pol == 1) return coop(0, count);
         // Measured: two lanes per operand pay for >= 3072-bit operands at low

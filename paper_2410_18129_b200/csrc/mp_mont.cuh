@@ -40,14 +40,19 @@ MPB_DEVI char* chunk_addr(const char* p, uint32_t idx, uint32_t sb) {
     asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(a) : "r"(idx), "r"(sb), "l"(reinterpret_cast<uint64_t>(p)));
     return reinterpret_cast<char*>(a);
 }
+// tm (optional): the TMA tensor map describing the whole array (bits 0..3: map index + 1, 0 = none)
+// and this view's first chunk row in it (bits 4..31); see k_modexp / TmaMaps in kernels.cuh.
 struct Arr {
     char* p;
     uint32_t sb;
+    uint32_t tm;
     MPB_DEVI uint4* addr(int q) const { return reinterpret_cast<uint4*>(chunk_addr(p, (uint32_t)q, sb)); }
     MPB_DEVI uint4 ld(int q) const { return *addr(q); }
     MPB_DEVI uint4 ld_stream(int q) const { return __ldcs(addr(q)); }  // evict-first (table scans)
     MPB_DEVI void st(int q, uint4 v) const { *addr(q) = v; }
-    MPB_DEVI Arr at(int chunk) const { return Arr{p + (size_t)(uint32_t)chunk * sb, sb}; }
+    MPB_DEVI Arr at(int chunk) const {
+        return Arr{p + (size_t)(uint32_t)chunk * sb, sb, tm + ((uint32_t)chunk << 4)};
+    }
 };
 
 // Per-thread shared-memory staging for the operand blocks of the next block product
@@ -56,7 +61,39 @@ struct Arr {
 struct Stage {
     uint32_t base;
     uint32_t cs;
+    // TMA path (engine<.., TMA = true>): this warp's tile stage, its two mbarriers, the warp's first
+    // operand index and the kernel's tensor maps
+    uint32_t tbase;
+    uint32_t tbar;
+    uint32_t kw;
+    uint32_t amask;  // the warp's active lanes
+    const void* maps;
 };
+// ---- TMA (cp.async.bulk.tensor) + mbarrier primitives
+MPB_DEVI void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+MPB_DEVI void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+MPB_DEVI void mbar_wait(uint32_t bar, uint32_t phase) {
+    uint32_t ok;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(bar), "r"(phase)
+            : "memory");
+    } while (!ok);
+}
+// 2-D tile of a word-sliced array: c0 = word offset (4 x operand index), c1 = chunk row
+MPB_DEVI void tma_load_2d(uint32_t dst, const void* map, int c0, int c1, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            dst),
+        "l"(map), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
 // Threads per CTA of every engine kernel (kernels.cuh kThreads): the stage stride blockDim * 16
 // is then a compile-time constant and every staging address is base + immediate.
 #ifdef MPB_THREADS
@@ -180,9 +217,13 @@ MPB_DEVI void final_select(int NB, const Arr& T, const Arr& OUT, uint32_t ctop, 
 enum { PH_MUL = 0, PH_SQR = 1, PH_Q = 2, PH_HI = 3 };
 enum { OP_MUL = 0, OP_MUL2 = 1, OP_SQR = 2, OP_LO = 3, OP_HI = 4 };
 
-template <int C, bool TRUNC>
+// TMA: the operand blocks of a pair are loaded per WARP as 2-D tiles (C/4 chunk rows x 32 operands
+// = (C/4) * 512 bytes) by one lane with cp.async.bulk.tensor, completing on the warp's mbarrier for
+// that buffer; the pair walk is identical in every lane, so the tile coordinates are warp-uniform.
+// tph: the two buffers' mbarrier phase bits (carried across calls).
+template <int C, bool TRUNC, bool TMA = false>
 MPB_DEVI void engine(int ph, int NB, const Arr& AX, const Arr& AY, const Arr& DST, const Arr& T, const Arr& N,
-                     const Arr& OUT, uint32_t& orlo, uint32_t& tl1, const Stage& sg) {
+                     const Arr& OUT, uint32_t& orlo, uint32_t& tl1, const Stage& sg, uint32_t* tph = nullptr) {
     uint32_t W[2 * C + 1];
     w_zero<C>(W);
     uint32_t carry = 0, borrow = 0;
@@ -223,16 +264,42 @@ MPB_DEVI void engine(int ph, int NB, const Arr& AX, const Arr& AY, const Arr& DS
     const char* const axp = AX.p;
     const char* const ayp = AY.p;
     const uint32_t sbx = AX.sb, sby = AY.sb;  // arrays may hold different operand counts
+    constexpr uint32_t kTile = (C / 4) * 512u;  // one operand block of 32 operands
+    const uint32_t lane = threadIdx.x & 31u;
+    if constexpr (TMA) {
+        // AX / AY were written (generic proxy) by earlier phases of this warp; make those writes
+        // visible to the async proxy before the first tile load of this phase
+        asm volatile("fence.proxy.async;" ::: "memory");
+        __syncwarp(sg.amask);
+    }
     auto issue = [&](int kk, int ss, int buf) {
-        const uint32_t b = sg.base + (uint32_t)(buf * 2 * (C / 4)) * kStageCS;
-        const uint32_t cx = (uint32_t)ss * (C / 4), cy = (uint32_t)(kk - ss) * (C / 4);
+        if constexpr (TMA) {
+            const bool dg = sqr && 2 * ss == kk;
+            const uint32_t dst = sg.tbase + (uint32_t)buf * 2u * kTile;
+            const uint32_t bar = sg.tbar + (uint32_t)buf * 8u;
+            __syncwarp(sg.amask);  // every lane has read this buffer's previous tiles (two pairs ago)
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_arrive_tx(bar, dg ? kTile : 2u * kTile);
+                const char* maps = static_cast<const char*>(sg.maps);
+                tma_load_2d(dst, maps + ((AX.tm & 15u) - 1u) * 128u, (int)(4u * sg.kw),
+                            (int)((AX.tm >> 4) + (uint32_t)ss * (C / 4)), bar);
+                if (!dg)
+                    tma_load_2d(dst + kTile, maps + ((AY.tm & 15u) - 1u) * 128u, (int)(4u * sg.kw),
+                                (int)((AY.tm >> 4) + (uint32_t)(kk - ss) * (C / 4)), bar);
+            }
+        } else {
+            const uint32_t b = sg.base + (uint32_t)(buf * 2 * (C / 4)) * kStageCS;
+            const uint32_t cx = (uint32_t)ss * (C / 4), cy = (uint32_t)(kk - ss) * (C / 4);
 #pragma unroll
-        for (int q = 0; q < C / 4; q++) cp_async16(b + q * kStageCS, chunk_addr(axp, cx + q, sbx));
-        if (!(sqr && 2 * ss == kk)) {
+            for (int q = 0; q < C / 4; q++) cp_async16(b + q * kStageCS, chunk_addr(axp, cx + q, sbx));
+            if (!(sqr && 2 * ss == kk)) {
 #pragma unroll
-            for (int q = 0; q < C / 4; q++) cp_async16(b + (C / 4 + q) * kStageCS, chunk_addr(ayp, cy + q, sby));
+                for (int q = 0; q < C / 4; q++)
+                    cp_async16(b + (C / 4 + q) * kStageCS, chunk_addr(ayp, cy + q, sby));
+            }
+            cp_commit();
         }
-        cp_commit();
     };
     int k = k0, s = k0 - NB + 1 > 0 ? k0 - NB + 1 : 0;
     int s_hi = sqr ? (k >> 1) : (k < NB - 1 ? k : NB - 1);
@@ -248,26 +315,37 @@ MPB_DEVI void engine(int ph, int NB, const Arr& AX, const Arr& AY, const Arr& DS
             ns_hi = sqr ? (nk >> 1) : (nk < NB - 1 ? nk : NB - 1);
         }
         const bool more = nk < k1;
-        if (more) {
-            issue(nk, ns, buf ^ 1);
-            cp_wait<1>();
+        if constexpr (TMA) {
+            if (more) issue(nk, ns, buf ^ 1);
+            mbar_wait(sg.tbar + (uint32_t)buf * 8u, (*tph >> buf) & 1u);
+            *tph ^= 1u << buf;
         } else {
-            cp_wait<0>();
+            if (more) {
+                issue(nk, ns, buf ^ 1);
+                cp_wait<1>();
+            } else {
+                cp_wait<0>();
+            }
         }
         const int t = k - s;
         const bool diag = sqr && s == t;
         uint32_t x[C], y[C];
         {
-            const uint32_t b = sg.base + (uint32_t)(buf * 2 * (C / 4)) * kStageCS;
+            // cp.async stage: chunk c of this thread at base + c * kStageCS; TMA tile: row c of the
+            // warp's tile, this lane's 16 bytes at + lane * 16 (both conflict-free LDS.128)
+            const uint32_t b = TMA ? sg.tbase + (uint32_t)buf * 2u * kTile + lane * 16u
+                                   : sg.base + (uint32_t)(buf * 2 * (C / 4)) * kStageCS;
+            constexpr uint32_t rs = TMA ? 512u : kStageCS;
+            constexpr uint32_t yo = TMA ? kTile : (C / 4) * kStageCS;
 #pragma unroll
             for (int q = 0; q < C / 4; q++) {
-                const uint4 v = lds128(b + q * kStageCS);
+                const uint4 v = lds128(b + q * rs);
                 x[4 * q] = v.x; x[4 * q + 1] = v.y; x[4 * q + 2] = v.z; x[4 * q + 3] = v.w;
             }
             if (!diag) {
 #pragma unroll
                 for (int q = 0; q < C / 4; q++) {
-                    const uint4 v = lds128(b + (C / 4 + q) * kStageCS);
+                    const uint4 v = lds128(b + yo + q * rs);
                     y[4 * q] = v.x; y[4 * q + 1] = v.y; y[4 * q + 2] = v.z; y[4 * q + 3] = v.w;
                 }
             }
@@ -355,9 +433,9 @@ MPB_DEVI void engine(int ph, int NB, const Arr& AX, const Arr& AY, const Arr& DS
 //   mode REDC: OUT = T*R^-1 mod N for the 2L-word T already in scratch T
 enum { MODE_MUL = 0, MODE_SQR = 1, MODE_REDC = 2 };
 
-template <int C, bool TRUNC>
+template <int C, bool TRUNC, bool TMA = false>
 MPB_DEVI void mont_op(int mode, int NB, const Arr& X, const Arr& B, const Arr& N, const Arr& NP, const Arr& T, const Arr& Q,
-                      const Arr& OUT, const Stage& sg) {
+                      const Arr& OUT, const Stage& sg, uint32_t* tph = nullptr) {
     uint32_t orlo = 0, tl1 = 0;
 #pragma unroll 1
     for (int step = mode == MODE_REDC ? 1 : 0; step < 3; step++) {
@@ -365,7 +443,7 @@ MPB_DEVI void mont_op(int mode, int NB, const Arr& X, const Arr& B, const Arr& N
         const Arr ax = step == 0 ? X : (step == 1 ? T : Q);
         const Arr ay = step == 0 ? B : (step == 1 ? NP : N);
         const Arr dst = step == 0 ? T : Q;
-        engine<C, TRUNC>(ph, NB, ax, ay, dst, T, N, OUT, orlo, tl1, sg);
+        engine<C, TRUNC, TMA>(ph, NB, ax, ay, dst, T, N, OUT, orlo, tl1, sg, tph);
     }
 }
 

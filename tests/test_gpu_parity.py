@@ -489,17 +489,18 @@ for bits, count, w, redc in ((1024, 9, 5, 1), (2048, 5, 4, 0), (3072, 4, 5, 1), 
 """
 
 
-@pytest.mark.parametrize("coop", ["0", "1"])
+@pytest.mark.parametrize("coop", ["0", "1", "tma"])
 def test_modexp_one_thread_and_two_lane_kernels(mpb, coop):
-    """Both exponentiation kernels, forced by MPB_COOP in a subprocess (the policy is read once per
-    process): one thread per operand (0) and two lanes per operand (1, mp_coop.cuh), 1024..4108 bits,
-    truncated and full REDC, against the oracle."""
+    """All three exponentiation kernels, forced by MPB_COOP / MPB_TMA in a subprocess (the policy is
+    read once per process): one thread per operand (0), two lanes per operand (1, mp_coop.cuh) and
+    one thread per operand with per-warp TMA operand tiles (tma), 1024..4108 bits, truncated and
+    full REDC, against the oracle."""
     import os
     import subprocess
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, MPB_COOP=coop)
+    env = dict(os.environ, MPB_COOP="0", MPB_TMA="1") if coop == "tma" else dict(os.environ, MPB_COOP=coop)
     res = subprocess.run([sys.executable, "-c", _COOP_SCRIPT % root], env=env, capture_output=True, text=True,
                          timeout=600)
     assert res.returncode == 0, res.stderr[-2000:]
