@@ -513,3 +513,36 @@ def test_modexp_one_thread_and_two_lane_kernels(mpb, coop):
         got = np.frombuffer(bytes.fromhex(hx), dtype=np.uint32).reshape(count, L)
         N, base, exp = I.modexp_inputs(config=4, count=count, bits=bits)
         assert np.array_equal(got, O.batch_modexp(base, exp, bits, N)), (bits, coop)
+
+
+# ----------------------------------------------------------------------- fuzz
+def test_fuzz_shapes(mpb):
+    """Seeded random shapes: widths 64..8192 bits (every block size C = 16, 12, 8, 4 and odd block
+    counts), ragged counts, windows 1..6, all REDC modes and product algorithms, against the
+    oracle.  Sizes are bounded so the oracle side stays within seconds."""
+    rng = random.Random(20241018)
+    cases = 0
+    for _ in range(24):
+        bits = rng.choice([64, 96, 160, 288, 416, 544, 700, 1056, 1312, 1600, 2112, 2720, 3200, 4000, 5000, 8192])
+        L = I.limbs_for_bits(bits)
+        count = rng.randint(1, 70)
+        w = rng.randint(1, 6)
+        redc = rng.choice(REDC)
+        algo = rng.choice([0, 1, 2, 3]) if redc != 2 else rng.choice([0, 1])
+        N, base, exp = I.modexp_inputs(config=3, count=count, bits=bits, dataset=cases)
+        dN = mpb.to_device(N)
+        Np, R2 = mpb.mont_batch_setup(dN, bits)
+        idx = sorted(rng.sample(range(count), min(count, 3 if bits <= 2048 else 1)))
+        a = mpb.to_device(base)
+        mm = mpb.to_host(mpb.mont_batch_mul(a, a, dN, Np, bits, redc=redc))
+        assert np.array_equal(mm[idx], O.batch_montmul(base[idx], base[idx], N[idx])), (bits, count, redc)
+        if bits <= 4000:
+            out = mpb.to_host(mpb.mont_batch_modexp_ct(dN, Np, R2, a, mpb.to_device(exp), bits, window=w, redc=redc,
+                                                       algo=algo))
+            assert np.array_equal(out[idx], O.batch_modexp(base[idx], exp[idx], bits, N[idx])), \
+                (bits, count, w, redc, algo)
+        prod = mpb.to_host(mpb.mp_batch_mul(a, a, bits, rng.choice([1, 2, 3])))
+        for k in idx:
+            assert I.from_limbs(prod[k]) == I.from_limbs(base[k]) ** 2, (bits, k)
+        cases += 1
+    assert cases == 24
