@@ -301,16 +301,20 @@ MPB_DEVI void acc_mul2(uint32_t (&W)[2 * C + 1], const uint32_t (&x)[C], const u
 // not depend on the off-diagonal rows, so ptxas can overlap them) and S the off-diagonal sum.
 template <int C>
 MPB_DEVI void acc_sqr(uint32_t (&W)[2 * C + 1], const uint32_t (&x)[C]) {
-    {
-        uint32_t D[2 * C];
-#pragma unroll
-        for (int i = 0; i < C; i++) pr_set(D[2 * i], D[2 * i + 1], x[i], x[i]);
-        w_add<0, 2 * C, 0>(W, D);
-    }
     uint32_t E[2 * C], O[2 * C];
     bp_sqr_offdiag<C>(x, E, O);
     fold_odd<C>(E, O);  // S = sum_{i<j} x_i x_j 2^{32(i+j)} < 2^{64C-1}
-    w_add_double<C>(W, E);
+    // E = 2S (funnel shifts, top down, in place; 2S < 2^{64C}), then + the diagonal squares x_i^2
+    // at the even-aligned pairs (2i, 2i+1) as ONE fused carry chain: 2S + D = x^2 < 2^{64C}, so the
+    // chain ends without a carry; one merge into the window
+#pragma unroll
+    for (int k = 2 * C - 1; k >= 1; k--) E[k] = __funnelshift_l(E[k - 1], E[k], 1);
+    E[0] <<= 1;
+    pr_first(E[0], E[1], x[0], x[0]);
+#pragma unroll
+    for (int i = 1; i < C - 1; i++) pr_next(E[2 * i], E[2 * i + 1], x[i], x[i]);
+    pr_next_end(E[2 * C - 2], E[2 * C - 1], x[C - 1], x[C - 1]);
+    w_add<0, 2 * C, 0>(W, E);
 }
 // W[0..C) += x*y mod 2^{32C}
 template <int C>
