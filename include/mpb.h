@@ -117,8 +117,9 @@ int rsa_batch_crt_ct(const uint32_t* c, const uint32_t* p, const uint32_t* q, co
 size_t rsa_batch_crt_workspace(size_t count, int bits, int window);
 
 /* End-to-end convenience over HOST buffers (operand-major, L limbs each; exp L limbs):
- * allocates device memory, copies in, runs setup + modexp, copies out, synchronises.
- * Returns MPB_OK or an error; blocking. */
+ * allocates device memory (stream-ordered, from the device's default memory pool, whose
+ * release threshold it raises so that repeated calls reuse the allocation), copies in, runs
+ * setup + modexp, copies out, synchronises.  Returns MPB_OK or an error; blocking. */
 int mpb_modexp_host(const uint32_t* N, const uint32_t* base, const uint32_t* exp, uint32_t* out, size_t count,
                     int bits, int window, int redc, void* stream);
 
