@@ -18,8 +18,7 @@
  *
  * Calls.  All pointers are DEVICE pointers, 16-byte aligned, owned by the caller; the library
  * never allocates or frees them and keeps no state between calls except the thread-local
- * error string and, created on first use, one auxiliary stream and two events per device and
- * host thread (mont_batch_modexp_ct runs a cooperative tail on it, joined back to `stream`).  Work is enqueued on `stream` (a cudaStream_t, 0 = legacy default) and the
+ * error string.  Work is enqueued on `stream` (a cudaStream_t, 0 = legacy default) and the
  * call returns immediately; kernel faults surface at the caller's next synchronisation.
  * count == 0 is a no-op returning MPB_OK.  Outputs must not alias inputs.
  *
@@ -91,8 +90,7 @@ size_t mont_batch_workspace(size_t count, int bits);
  * exp has L limbs and `bits` significant bits (zero padded); timing depends on
  * (count, bits, window, redc) only.  window in 1..6.  exp = 0 gives 1 (0^0 = 1).
  * For >= 3072-bit operands, batches below a quarter of the device's resident capacity run with
- * two lanes per operand, and the partial last wave of larger batches runs that way concurrently
- * with the final whole wave (the result is the same; only the schedule differs). */
+ * two lanes per operand (the result is the same; only the schedule differs). */
 int mont_batch_modexp_ct(const uint32_t* N, const uint32_t* Nprime, const uint32_t* R2, const uint32_t* base,
                          const uint32_t* exp, uint32_t* out, size_t count, int bits, int window, int redc,
                          int algo, void* workspace, size_t workspace_bytes, void* stream);

@@ -517,30 +517,8 @@ void Launch<C>::mont_redc(const uint32_t* T, const uint32_t* N, const uint32_t* 
     if (trunc) k_mont_redc<C, true><<<grid_for(count), kThreads, sm, s>>>(T, N, NP, c, count, nb, ws);
     else k_mont_redc<C, false><<<grid_for(count), kThreads, sm, s>>>(T, N, NP, c, count, nb, ws);
 }
-// Split of a batch between the one-thread kernel (whole waves) and the cooperative kernel
-// (small batches, partial last wave); MPB_COOP=0 / 1 forces never / always (tuning and tests).
-// A per-thread, per-device auxiliary stream and fork/join events (created once, never destroyed).
-inline bool aux_stream(cudaStream_t* s2, cudaEvent_t* fork, cudaEvent_t* join) {
-    struct Aux {
-        int dev = -1;
-        cudaStream_t s = nullptr;
-        cudaEvent_t f = nullptr, j = nullptr;
-    };
-    thread_local Aux aux[16];
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return false;
-    Aux& a = aux[dev];
-    if (a.dev != dev) {
-        if (cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking) != cudaSuccess) return false;
-        if (cudaEventCreateWithFlags(&a.f, cudaEventDisableTiming) != cudaSuccess) return false;
-        if (cudaEventCreateWithFlags(&a.j, cudaEventDisableTiming) != cudaSuccess) return false;
-        a.dev = dev;
-    }
-    *s2 = a.s;
-    *fork = a.f;
-    *join = a.j;
-    return true;
-}
+// One-thread or cooperative kernel (small >= 3072-bit batches); MPB_COOP=0 / 1 forces never /
+// always (tuning and tests).
 // TMA tensor map of a word-sliced array: 2-D, dim 0 = 4*count uint32 words (all operands' chunk
 // rows), dim 1 = rows (chunks per operand), row stride count*16 bytes; box = 128 words (one warp's
 // 32 operands) x box_rows (one block); out-of-range operands read as zero.
@@ -657,25 +635,8 @@ void Launch<C>::modexp(const uint32_t* N, const uint32_t* NP, const uint32_t* R2
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_modexp<C, 1, NBT, 0>, kThreads, sm);
         const size_t slots = (size_t)sms * (size_t)(per_sm > 0 ? per_sm : 1) * kThreads;
         if (4 * count <= slots) return coop(0, count);  // small batch
-        const size_t tail = count % slots;
-        if (count > slots && tail > 0 && 4 * tail <= slots) {
-            // whole waves on `s`; the cooperative tail on a second stream, launched after them so its
-            // CTAs take the slots the last wave frees (fork / join with events: still asynchronous)
-            cudaStream_t s2;
-            cudaEvent_t fork, join;
-            if (aux_stream(&s2, &fork, &join)) {
-                cudaEventRecord(fork, s);
-                cudaStreamWaitEvent(s2, fork, 0);
-                single(0, count - tail);
-                cudaStream_t keep = s;
-                s = s2;
-                coop(count - tail, tail);
-                s = keep;
-                cudaEventRecord(join, s2);
-                cudaStreamWaitEvent(s, join, 0);
-                return;
-            }
-        }
+        // (a cooperative tail after the whole waves measured neutral at 2^16 x 4096 bits: the
+        // one-thread tail already overlaps the drain of the last wave)
         single(0, count);
     });
 }
