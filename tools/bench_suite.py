@@ -193,6 +193,35 @@ def rsa_crt(bits, count, reps, n_keys=16):
     torch.cuda.empty_cache()
 
 
+def config5_e2e(bits=2048, count=1 << 22, window=5):
+    """Config 5 end to end on one GPU: mpb_modexp_host over PINNED host buffers --
+    H2D of N / base / exp, layout expand, setup, modexp, contract, D2H -- timed by the host clock
+    around the blocking call (one untimed warm-up call sizes the memory pool)."""
+    import ctypes
+
+    N, base, exp = I.modexp_inputs(config=5, count=count, bits=bits)
+    hN, hB, hE = (torch.from_numpy(x.view(np.int32)).pin_memory() for x in (N, base, exp))
+    hO = torch.empty_like(hN).pin_memory()
+    stream = torch.cuda.current_stream()
+
+    def call():
+        rc = mpb._lib.mpb_modexp_host(hN.data_ptr(), hB.data_ptr(), hE.data_ptr(), hO.data_ptr(), count, bits, window,
+                                      1, ctypes.c_void_p(stream.cuda_stream))
+        assert rc == 0, mpb._lib.mpb_last_error()
+
+    call()
+    t0 = time.perf_counter()
+    call()
+    dt = time.perf_counter() - t0
+    out = hO.numpy().view(np.uint32)
+    idx = sample_idx(count, 8, seed=5)
+    ok = bool(np.array_equal(out[idx], O.batch_modexp(base[idx], exp[idx], bits, N[idx])))
+    L = I.limbs_for_bits(bits)
+    emit({"config": 5, "op": "modexp_e2e_pinned", "bits": bits, "count": count, "window": window, "s": dt,
+          "modexp_per_s": count / dt, "h2d_bytes": 3 * count * L * 4, "d2h_bytes": count * L * 4,
+          "parity_sample": ok})
+
+
 def paper_protocol(bits=2048, count=1 << 18, datasets=5, launches=10, warmup=3):
     """SURVEY 8(d) timing protocol, adapted from P:L614-621: 3 warm-up launches, then for each of
     D = 5 seeded datasets the minimum over 10 launches (CUDA events around the kernel only);
@@ -247,6 +276,7 @@ def main():
         products(4154, 1 << 16, args.reps)
     if 5 in cfgs:
         modexp_run(5, 2048, 1 << 22, 1, redcs=((1, "truncated"),), check=64)
+        config5_e2e()
     if 7 in cfgs:  # the paper's timing statistic on config 3
         paper_protocol()
     if 6 in cfgs:  # CRT-RSA (not a BASELINE config: SURVEY 8(f) f4)
