@@ -269,8 +269,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_modexp_tma(
                                             0xFFFFFFFFu, &maps);
 }
 
-// Two lanes per operand (mp_coop.cuh): for batches below half the resident capacity and for the
-// partial last wave of larger ones.
+// Two lanes per operand (mp_coop.cuh): for >= 3072-bit batches below a quarter of the resident
+// capacity (Launch::modexp).
 template <int C, int RM, int NBT>
 __global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_modexp_coop(
     const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP, const uint32_t* __restrict__ R2,
@@ -627,7 +627,7 @@ void Launch<C>::modexp(const uint32_t* N, const uint32_t* NP, const uint32_t* R2
         }
         if (redc == 2 || levels > 0 || pol == 0) return single(0, count);
         if (pol == 1) return coop(0, count);
-        // Measured (DESIGN.md 5.5): two lanes per operand pay for >= 3072-bit operands at low
+        // Measured (DESIGN.md 5.5b): two lanes per operand pay for >= 3072-bit operands at low
         // occupancy (1.23x at 4096 bits); at 1024/2048 bits or near half occupancy they do not.
         if (C * nb < 96) return single(0, count);
         int dev = 0, sms = 148, per_sm = min_blocks<C>();
