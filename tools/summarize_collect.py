@@ -40,6 +40,15 @@ d = {"kernel": "k_modexp<16,1,4,0>",
      "warps_active_pct": round(g("sm__warps_active.avg.pct_of_peak_sustained_active"), 2),
      "l2_hit_pct": round(g("lts__t_sector_hit_rate.pct"), 2), "l1_hit_pct": round(g("l1tex__t_sector_hit_rate.pct"), 2),
      "stalls_per_issue": st, "warp_instructions": g("smsp__inst_executed.sum")}
+pipes = {}
+for name in ("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
+             "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+             "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+             "sm__issue_active.avg.pct_of_peak_sustained_elapsed",
+             "smsp__sass_inst_executed_op_local_ld.sum", "smsp__sass_inst_executed_op_local_st.sum"):
+    if name in hdr:
+        pipes[name] = g(name)
+d["pipes"] = pipes
 lines = [l for l in open(f"{G}/launches.csv").read().splitlines() if l.startswith('"') and "gpu__time_duration" in l]
 tot = collections.Counter()
 for l in csv.reader(lines):
