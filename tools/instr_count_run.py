@@ -4,7 +4,8 @@ import sys
 sys.path.insert(0, "/root/repo")
 import torch
 from paper_2410_18129_b200 import inputs as I, mpb
-bits, count = 2048, 56832
+import os
+bits, count = int(os.environ.get("BITS", "2048")), 56832
 a, b = I.mul_inputs(config=4, count=count, bits=bits)
 da, db = mpb.to_device(a), mpb.to_device(b)
 N, x, y = I.montmul_inputs(config=2, count=count, bits=bits)
