@@ -108,7 +108,8 @@ size_t mont_batch_setup_workspace(size_t count, int bits);
  * mpb_limbs(bits) limbs, p, q, dp, dq, qinv have mpb_limbs(bits/2) limbs (word-sliced, `count`
  * operands each).  Preconditions (not checked on the device): p, q odd with exactly bits/2 bits,
  * qinv = q^-1 mod p, c < p*q, dp, dq < 2^(bits/2).  redc selects the REDC mode of the
- * exponentiation.  workspace: rsa_batch_crt_workspace(count, bits, window) bytes. */
+ * exponentiation.  workspace: rsa_batch_crt_workspace(count, bits, window) bytes.
+ * MPB_EUNSUPPORTED for count > 2^26 (the half-size exponentiation runs 2*count operands). */
 int rsa_batch_crt_ct(const uint32_t* c, const uint32_t* p, const uint32_t* q, const uint32_t* dp, const uint32_t* dq,
                      const uint32_t* qinv, uint32_t* m, size_t count, int bits, int window, int redc,
                      void* workspace, size_t workspace_bytes, void* stream);

@@ -344,7 +344,8 @@ int rsa_batch_crt_ct(const uint32_t* c, const uint32_t* p, const uint32_t* q, co
     if (int rc = limbs_checked(bits, L)) return rc;
     if (int rc = limbs_checked(bits / 2, Lh)) return rc;
     if (count == 0) return MPB_OK;
-    if (count > kMaxCount) return fail(MPB_EUNSUPPORTED, "count exceeds 2^27 operands per call");
+    if (count > kMaxCount / 2)  // the half-size modexp runs 2 * count operands in one call
+        return fail(MPB_EUNSUPPORTED, "count exceeds 2^26 RSA operations per call");
     if (int rc = check_ptrs({c, p, q, dp, dq, qinv, m, ws})) return rc;
     for (const void* in : {(const void*)c, (const void*)p, (const void*)q, (const void*)dp, (const void*)dq,
                            (const void*)qinv})

@@ -108,3 +108,9 @@ def test_host_side_argument_checks(lib):
     assert lib.mont_batch_modexp_ct(None, None, None, None, None, None, 4, 1024, 5, 1, 9, None, 0, None) == EINVAL
     assert lib.mont_batch_modexp_ct(None, None, None, None, None, None, big, 1024, 5, 1, 0, None, 0, None) \
         == EUNSUPPORTED
+    # CRT-RSA runs 2 * count half-size operands in one exponentiation: at most 2^26 per call
+    lib.rsa_batch_crt_ct.argtypes = [vp, vp, vp, vp, vp, vp, vp, sz, i, i, i, vp, sz, vp]
+    crt_big = (1 << 26) + 1
+    assert lib.rsa_batch_crt_ct(None, None, None, None, None, None, None, crt_big, 2048, 5, 1, None, 0, None) \
+        == EUNSUPPORTED
+    assert b"2^26" in lib.mpb_last_error()
