@@ -261,7 +261,11 @@ size_t mont_batch_modexp_ct_workspace(size_t count, int bits, int window, int al
     if (L <= 0 || window < 1 || window > 6) return 0;
     const int C = block_of(L);
     const size_t kara = (size_t)mpb::kara_scratch_blocks_host(L / C, kara_levels(algo, L)) * C;
-    return count * ((size_t)L * (size_t)((1 << window) + 5) + kara) * sizeof(uint32_t);
+    // word-sliced layout (Karatsuba products, TMA tiles): G | Y | T | Q | S | scratch, stride count;
+    // warp-tiled layout (the default path): G | Y | T | Q | S | N | N' over count rounded up to 32
+    const size_t sliced = count * ((size_t)L * (size_t)((1 << window) + 5) + kara);
+    const size_t tiled = ((count + 31) & ~(size_t)31) * (size_t)L * (size_t)((1 << window) + 7);
+    return (sliced > tiled ? sliced : tiled) * sizeof(uint32_t);
 }
 
 int mont_batch_modexp_ct(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,

@@ -148,39 +148,88 @@ __global__ void __launch_bounds__(kThreads) k_mont_redc(const uint32_t* __restri
 //   then per window j = W-2 .. 0:  w x Y = MontSqr(Y),  S = CTsel(G, window j)
 //                                  (P:L765-766),  Y = MontMul(Y, S)
 //   last op          out = REDC(Y)
-// workspace per operand (word-sliced, stride count): G (2^w * L) | Y (L) | T (2L) | Q (L) | S (L)
-//   | Karatsuba scratch (kara_scratch_blocks(nb, KLEV) blocks; KLEV = algo levels for the products)
+// workspace: TILE (schoolbook products, cp.async staging -- the default path): warp-tiled arrays
+// (ArrT, DESIGN 5.6) over cpad = count rounded up to 32 operands:
+//   G (2^w * L) | Y (L) | T (2L) | Q (L) | S (L) | N (L) | N' (L)
+// with N, N', base and R^2 copied in from the word-sliced inputs and the result copied out, so
+// every engine array has the compile-time chunk stride.  Otherwise (Karatsuba products, TMA
+// tiles): word-sliced arrays, stride count: G | Y | T | Q | S | Karatsuba scratch
+// (kara_scratch_blocks(nb, KLEV) blocks; KLEV = algo levels for the products).
 // The whole exponentiation of operand k (of `count`, the arrays' stride).  COOP: two lanes per
 // operand (mp_coop.cuh), role = lane & 1, mask = the active pairs of the warp.
+__host__ __device__ constexpr bool modexp_tiled(int KLEV, bool TMA) { return KLEV == 0 && !TMA; }
+// warp-tiled view of operand k in an array of nch chunks per operand
+MPB_DEVI ArrT tarr(uint32_t* base, int nch, size_t k) {
+    char* p = reinterpret_cast<char*>(base) + (k >> 5) * ((size_t)nch * kTileSB) + (k & 31) * 16;
+    return ArrT{p, kTileSB, 0u};
+}
 template <int C, int RM, int NBT, int KLEV, bool COOP, bool TMA = false>
 MPB_DEVI void modexp_body(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
                           const uint32_t* exp, uint32_t* out, size_t count, size_t k, int nb_rt, int bits, int w,
                           uint32_t* ws, uint32_t role, unsigned mask, const TmaMaps* maps = nullptr) {
+    constexpr bool TILE = modexp_tiled(KLEV, TMA);
+    using A = std::conditional_t<TILE, ArrT, Arr>;
     const int nb = NBT ? NBT : nb_rt;  // compile-time block count for the hot sizes
     const int L = C * nb, Q4 = L / 4;
     const int nent = 1 << w;
-    uint32_t* p = ws;
-    const Arr G = arr(p, count, k);
-    p += (size_t)nent * L * count;
-    const Arr Y = arr(p, count, k);
-    p += (size_t)L * count;
-    const Arr T = arr(p, count, k);
-    p += (size_t)2 * L * count;
-    const Arr Q = arr(p, count, k);
-    p += (size_t)L * count;
-    const Arr S = arr(p, count, k);
-    p += (size_t)L * count;
-    const Arr KS = arr(p, count, k);  // Karatsuba scratch (KLEV > 0)
     const Arr Nn = arr(N, count, k), NPn = arr(NP, count, k), R2n = arr(R2, count, k), Bn = arr(base, count, k);
     const Arr On = arr(out, count, k);
     Stage sg = stage();
     uint32_t tph = 0;  // TMA: mbarrier phase bits of the two tile buffers
-    Arr Gt = G, Yt = Y, Tt = T, Qt = Q, St = S, Nt = Nn, NPt = NPn, R2t = R2n, Bt = Bn;
-    if constexpr (TMA) {  // the same arrays, tagged with their tensor maps
-        sg = stage_tma<C>(k - (threadIdx.x & 31u), maps);
-        Gt.tm = TM_G; Yt.tm = TM_Y; Tt.tm = TM_T; Qt.tm = TM_Q; St.tm = TM_S;
-        Nt.tm = TM_N; NPt.tm = TM_NP; R2t.tm = TM_R2; Bt.tm = TM_BASE;
+    A Gt, Yt, Tt, Qt, St, Nt, NPt, R2t, Bt, KS;
+    if constexpr (TILE) {
+        const size_t cpad = (count + 31) & ~(size_t)31;
+        uint32_t* p = ws;
+        auto take = [&](int nch) {
+            const ArrT a = tarr(p, nch, k);
+            p += cpad * (size_t)nch * 4;
+            return a;
+        };
+        Gt = take(nent * Q4);
+        Yt = take(Q4);
+        Tt = take(2 * Q4);
+        Qt = take(Q4);
+        St = take(Q4);
+        Nt = take(Q4);
+        NPt = take(Q4);
+        KS = St;   // unused (schoolbook)
+        Bt = Yt;   // base, then Y
+        R2t = St;  // R^2, then S
+        if (!COOP || role == 0) {
+#pragma unroll 1
+            for (int q = 0; q < Q4; q++) {
+                Nt.st(q, Nn.ld(q));
+                NPt.st(q, NPn.ld(q));
+                Bt.st(q, Bn.ld(q));
+                R2t.st(q, R2n.ld(q));
+            }
+        }
+        if constexpr (COOP) __syncwarp(mask);
+    } else {
+        uint32_t* p = ws;
+        Gt = arr(p, count, k);
+        p += (size_t)nent * L * count;
+        Yt = arr(p, count, k);
+        p += (size_t)L * count;
+        Tt = arr(p, count, k);
+        p += (size_t)2 * L * count;
+        Qt = arr(p, count, k);
+        p += (size_t)L * count;
+        St = arr(p, count, k);
+        p += (size_t)L * count;
+        KS = arr(p, count, k);  // Karatsuba scratch (KLEV > 0)
+        Nt = Nn; NPt = NPn; R2t = R2n; Bt = Bn;
+        if constexpr (TMA) {  // the same arrays, tagged with their tensor maps
+            sg = stage_tma<C>(k - (threadIdx.x & 31u), maps);
+            Gt.tm = TM_G; Yt.tm = TM_Y; Tt.tm = TM_T; Qt.tm = TM_Q; St.tm = TM_S;
+            Nt.tm = TM_N; NPt.tm = TM_NP; R2t.tm = TM_R2; Bt.tm = TM_BASE;
+        }
     }
+    const A G = Gt, Y = Yt, T = Tt, Q = Qt;
+    // the result: word-sliced output directly, or (TILE) S then copied out
+    A Ofin;
+    if constexpr (TILE) Ofin = St;
+    else Ofin = On;
 
     const int nwin = (bits + w - 1) / w;
     const int per_win = w + 2;
@@ -190,7 +239,7 @@ MPB_DEVI void modexp_body(const uint32_t* N, const uint32_t* NP, const uint32_t*
         int mode = MODE_MUL;
         bool select = false;
         int win = 0;
-        Arr X = Yt, B = Yt, O = Yt;
+        A X = Yt, B = Yt, O = Yt;
         if (op == 0) {
             mode = MODE_REDC; X = R2t; O = Gt;
         } else if (op < nent) {
@@ -200,7 +249,7 @@ MPB_DEVI void modexp_body(const uint32_t* N, const uint32_t* NP, const uint32_t*
         } else if (op == nent) {
             select = true; win = nwin - 1; O = Yt;
         } else if (op == n_ops - 1) {
-            mode = MODE_REDC; X = Yt; O = On;
+            mode = MODE_REDC; X = Yt; O = Ofin;
         } else {
             const int r = (op - nent - 1) % per_win;
             win = nwin - 2 - (op - nent - 1) / per_win;
@@ -235,12 +284,19 @@ MPB_DEVI void modexp_body(const uint32_t* N, const uint32_t* NP, const uint32_t*
         }
         if constexpr (COOP) {
             static_assert(RM != 2 && KLEV == 0, "cooperative operands: truncated or full REDC, schoolbook");
-            mont_op_coop<C, RM == 1>(mode, nb, X, B, Nn, NPn, T, Q, O, sg, role, mask);
+            mont_op_coop<C, RM == 1>(mode, nb, X, B, Nt, NPt, T, Q, O, sg, role, mask);
         } else if constexpr (TMA) {
             static_assert(RM != 2 && KLEV == 0, "TMA operand tiles: truncated or full REDC, schoolbook");
             mont_op<C, RM == 1, true>(mode, nb, X, B, Nt, NPt, Tt, Qt, O, sg, &tph);
         } else {
-            mont_op_rm<C, RM, KLEV>(mode, nb, X, B, Nn, NPn, T, Q, O, KS, sg);
+            mont_op_rm<C, RM, KLEV>(mode, nb, X, B, Nt, NPt, T, Q, O, KS, sg);
+        }
+    }
+    if constexpr (TILE) {  // the result, S (warp tile) -> out (word-sliced)
+        if constexpr (COOP) __syncwarp(mask);
+        if (!COOP || role == 0) {
+#pragma unroll 1
+            for (int q = 0; q < Q4; q++) On.st(q, Ofin.ld(q));
         }
     }
 }

@@ -30,9 +30,9 @@ MPB_DEVI void coop_window_sum(uint32_t (&W)[2 * C + 1], unsigned mask) {
     add_end(W[2 * C], o[2 * C]);
 }
 
-template <int C, bool TRUNC>
-MPB_DEVI void engine_coop(int ph, int NB, const Arr& AX, const Arr& AY, const Arr& DST, const Arr& T, const Arr& N,
-                          const Arr& OUT, uint32_t& orlo, uint32_t& tl1, const Stage& sg, uint32_t role,
+template <int C, bool TRUNC, class AR = Arr>
+MPB_DEVI void engine_coop(int ph, int NB, const AR& AX, const AR& AY, const AR& DST, const AR& T, const AR& N,
+                          const AR& OUT, uint32_t& orlo, uint32_t& tl1, const Stage& sg, uint32_t role,
                           unsigned mask) {
     uint32_t W[2 * C + 1];
     w_zero<C>(W);
@@ -93,12 +93,24 @@ MPB_DEVI void engine_coop(int ph, int NB, const Arr& AX, const Arr& AY, const Ar
         bool valid, dg;
         pair_of(kk, it, ss, valid, dg);
         const uint32_t b = sg.base + (uint32_t)(buf * 2 * (C / 4)) * kStageCS;
-        const uint32_t cx = (uint32_t)ss * (C / 4), cy = (uint32_t)(kk - ss) * (C / 4);
+        if constexpr (AR::kSBC != 0) {  // warp tile: one address per block, immediate row offsets
+            const char* bx = reinterpret_cast<const char*>(AX.addr(ss * (C / 4)));
 #pragma unroll
-        for (int q = 0; q < C / 4; q++) cp_async16(b + q * kStageCS, chunk_addr(axp, cx + q, sbx));
-        if (!dg) {
+            for (int q = 0; q < C / 4; q++) cp_async16(b + q * kStageCS, bx + q * AR::kSBC);
+            if (!dg) {
+                const char* by = reinterpret_cast<const char*>(AY.addr((kk - ss) * (C / 4)));
 #pragma unroll
-            for (int q = 0; q < C / 4; q++) cp_async16(b + (C / 4 + q) * kStageCS, chunk_addr(ayp, cy + q, sby));
+                for (int q = 0; q < C / 4; q++) cp_async16(b + (C / 4 + q) * kStageCS, by + q * AR::kSBC);
+            }
+        } else {
+            const uint32_t cx = (uint32_t)ss * (C / 4), cy = (uint32_t)(kk - ss) * (C / 4);
+#pragma unroll
+            for (int q = 0; q < C / 4; q++) cp_async16(b + q * kStageCS, chunk_addr(axp, cx + q, sbx));
+            if (!dg) {
+#pragma unroll
+                for (int q = 0; q < C / 4; q++)
+                    cp_async16(b + (C / 4 + q) * kStageCS, chunk_addr(ayp, cy + q, sby));
+            }
         }
         cp_commit();
     };
@@ -226,16 +238,16 @@ MPB_DEVI void engine_coop(int ph, int NB, const Arr& AX, const Arr& AY, const Ar
     __syncwarp(mask);  // both lanes' stores are visible to both before the next phase
 }
 
-template <int C, bool TRUNC>
-MPB_DEVI void mont_op_coop(int mode, int NB, const Arr& X, const Arr& B, const Arr& N, const Arr& NP, const Arr& T,
-                           const Arr& Q, const Arr& OUT, const Stage& sg, uint32_t role, unsigned mask) {
+template <int C, bool TRUNC, class AR = Arr>
+MPB_DEVI void mont_op_coop(int mode, int NB, const AR& X, const AR& B, const AR& N, const AR& NP, const AR& T,
+                           const AR& Q, const AR& OUT, const Stage& sg, uint32_t role, unsigned mask) {
     uint32_t orlo = 0, tl1 = 0;
 #pragma unroll 1
     for (int step = mode == MODE_REDC ? 1 : 0; step < 3; step++) {
         const int ph = step == 0 ? (mode == MODE_SQR ? PH_SQR : PH_MUL) : (step == 1 ? PH_Q : PH_HI);
-        const Arr ax = step == 0 ? X : (step == 1 ? T : Q);
-        const Arr ay = step == 0 ? B : (step == 1 ? NP : N);
-        const Arr dst = step == 0 ? T : Q;
+        const AR ax = step == 0 ? X : (step == 1 ? T : Q);
+        const AR ay = step == 0 ? B : (step == 1 ? NP : N);
+        const AR dst = step == 0 ? T : Q;
         engine_coop<C, TRUNC>(ph, NB, ax, ay, dst, T, N, OUT, orlo, tl1, sg, role, mask);
     }
 }

@@ -161,9 +161,9 @@ namespace mpb {
 // Montgomery operation whose product phase (T = X*B or X^2) uses KLEV levels of block Karatsuba
 // (Karatsuba inside MontMul/MontSqr); the reduction phases stay on the engine.
 // KS: kara_scratch_blocks(NB, KLEV) blocks of scratch.  KLEV = 0 is mont_op.
-template <int C, bool TRUNC, int KLEV>
-MPB_DEVI void mont_op_k(int mode, int NB, const Arr& X, const Arr& B, const Arr& N, const Arr& NP, const Arr& T,
-                        const Arr& Q, const Arr& OUT, const Arr& KS, const Stage& sg) {
+template <int C, bool TRUNC, int KLEV, class AR = Arr>
+MPB_DEVI void mont_op_k(int mode, int NB, const AR& X, const AR& B, const AR& N, const AR& NP, const AR& T,
+                        const AR& Q, const AR& OUT, const AR& KS, const Stage& sg) {
     if constexpr (KLEV == 0) {
         mont_op<C, TRUNC>(mode, NB, X, B, N, NP, T, Q, OUT, sg);
     } else {
@@ -175,9 +175,9 @@ MPB_DEVI void mont_op_k(int mode, int NB, const Arr& X, const Arr& B, const Arr&
 // Any REDC mode: RM = 0 full (alg:8MontRed), 1 truncated (alg:trunc_montred), 2 CIOS
 // (alg:8BlockMontRed, schoolbook only: the reduction is interleaved with the product rows).
 // CIOS uses T as its Y scratch and Q as its m scratch; REDC(X) is MontMul(X, 1).
-template <int C, int RM, int KLEV>
-MPB_DEVI void mont_op_rm(int mode, int NB, const Arr& X, const Arr& B, const Arr& N, const Arr& NP, const Arr& T,
-                         const Arr& Q, const Arr& OUT, const Arr& KS, const Stage& sg) {
+template <int C, int RM, int KLEV, class AR = Arr>
+MPB_DEVI void mont_op_rm(int mode, int NB, const AR& X, const AR& B, const AR& N, const AR& NP, const AR& T,
+                         const AR& Q, const AR& OUT, const AR& KS, const Stage& sg) {
     if constexpr (RM == 2) {
         static_assert(KLEV == 0, "CIOS interleaves reduction and product rows: schoolbook only");
         cios_op<C>(NB, X, B, mode == MODE_REDC, N, NP, T, Q, OUT);

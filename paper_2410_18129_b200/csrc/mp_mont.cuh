@@ -42,18 +42,32 @@ MPB_DEVI char* chunk_addr(const char* p, uint32_t idx, uint32_t sb) {
 }
 // tm (optional): the TMA tensor map describing the whole array (bits 0..3: map index + 1, 0 = none)
 // and this view's first chunk row in it (bits 4..31); see k_modexp / TmaMaps in kernels.cuh.
-struct Arr {
+// SBC = 0: word-sliced array with the run-time stride sb (the ABI layout, DESIGN 5.6).
+// SBC = kTileSB: warp-tiled workspace array (the exponentiation's internal arrays, DESIGN 5.6):
+// the 32 operands of a warp tile keep chunk q of all 32 numbers in one 512-byte row, rows of one
+// tile contiguous, so chunk q of this thread's number is at p + q * 512 -- a compile-time stride,
+// and every chunk of a block is an immediate offset from one address.
+template <uint32_t SBC>
+struct ArrS {
+    static constexpr uint32_t kSBC = SBC;
     char* p;
     uint32_t sb;
     uint32_t tm;
-    MPB_DEVI uint4* addr(int q) const { return reinterpret_cast<uint4*>(chunk_addr(p, (uint32_t)q, sb)); }
+    MPB_DEVI uint4* addr(int q) const {
+        if constexpr (SBC != 0) return reinterpret_cast<uint4*>(p + (ptrdiff_t)q * (ptrdiff_t)SBC);
+        else return reinterpret_cast<uint4*>(chunk_addr(p, (uint32_t)q, sb));
+    }
     MPB_DEVI uint4 ld(int q) const { return *addr(q); }
     MPB_DEVI uint4 ld_stream(int q) const { return __ldcs(addr(q)); }  // evict-first (table scans)
     MPB_DEVI void st(int q, uint4 v) const { *addr(q) = v; }
-    MPB_DEVI Arr at(int chunk) const {
-        return Arr{p + (size_t)(uint32_t)chunk * sb, sb, tm + ((uint32_t)chunk << 4)};
+    MPB_DEVI ArrS at(int chunk) const {
+        if constexpr (SBC != 0) return ArrS{p + (ptrdiff_t)chunk * (ptrdiff_t)SBC, sb, tm};
+        else return ArrS{p + (size_t)(uint32_t)chunk * sb, sb, tm + ((uint32_t)chunk << 4)};
     }
 };
+constexpr uint32_t kTileSB = 512;  // one chunk row of a warp tile: 32 operands x 16 bytes
+using Arr = ArrS<0>;
+using ArrT = ArrS<kTileSB>;
 
 // Per-thread shared-memory staging for the operand blocks of the next block product
 // (double buffered, filled by cp.async while the current block product runs).
@@ -116,16 +130,16 @@ MPB_DEVI uint4 lds128(uint32_t saddr) {
     return v;
 }
 
-template <int C>
-MPB_DEVI void ldb(const Arr& a, int blk, uint32_t (&x)[C]) {
+template <int C, class AR = Arr>
+MPB_DEVI void ldb(const AR& a, int blk, uint32_t (&x)[C]) {
 #pragma unroll
     for (int q = 0; q < C / 4; q++) {
         uint4 v = a.ld(blk * (C / 4) + q);
         x[4 * q] = v.x; x[4 * q + 1] = v.y; x[4 * q + 2] = v.z; x[4 * q + 3] = v.w;
     }
 }
-template <int C, int N>
-MPB_DEVI void stb(const Arr& a, int blk, const uint32_t (&x)[N]) {
+template <int C, int N, class AR = Arr>
+MPB_DEVI void stb(const AR& a, int blk, const uint32_t (&x)[N]) {
     static_assert(N >= C, "");
 #pragma unroll
     for (int q = 0; q < C / 4; q++) a.st(blk * (C / 4) + q, make_uint4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]));
@@ -147,9 +161,9 @@ MPB_DEVI void w_shift(uint32_t (&W)[2 * C + 1]) {  // W >>= 32C
 // ------------------------------------------------ shared tail: C, D = C - N
 // Block j of H (window words 0..C-1) becomes block j of C = T_hi + H + carry (truncated) or
 // of C itself (full); C is parked in T block NB+j and D = C - N - borrow goes to OUT block j.
-template <int C>
-MPB_DEVI void emit_block(const uint32_t (&W)[2 * C + 1], int j, int NB, bool add_thi, const Arr& T, const Arr& N,
-                         const Arr& OUT, uint32_t& carry, uint32_t& borrow, bool wr = true) {
+template <int C, class AR = Arr>
+MPB_DEVI void emit_block(const uint32_t (&W)[2 * C + 1], int j, int NB, bool add_thi, const AR& T, const AR& N,
+                         const AR& OUT, uint32_t& carry, uint32_t& borrow, bool wr = true) {
     uint32_t c[C];
 #pragma unroll
     for (int i = 0; i < C; i++) c[i] = W[i];
@@ -173,8 +187,8 @@ MPB_DEVI void emit_block(const uint32_t (&W)[2 * C + 1], int j, int NB, bool add
 
 // OUT = (ctop || !borrow) ? D : C, with D in OUT and C in T[NB..2NB) -- a mask, no branch.
 // Two blocks per step so that 4*(C/4) loads are in flight (the data was just written: L2 latency).
-template <int C>
-MPB_DEVI void final_select(int NB, const Arr& T, const Arr& OUT, uint32_t ctop, uint32_t borrow, bool wr = true) {
+template <int C, class AR = Arr>
+MPB_DEVI void final_select(int NB, const AR& T, const AR& OUT, uint32_t ctop, uint32_t borrow, bool wr = true) {
     const uint32_t m = 0u - ((ctop | (borrow ^ 1u)) & 1u);  // all ones: take D = C - N
     constexpr int Q = C / 4;
 #pragma unroll 1
@@ -221,9 +235,9 @@ enum { OP_MUL = 0, OP_MUL2 = 1, OP_SQR = 2, OP_LO = 3, OP_HI = 4 };
 // = (C/4) * 512 bytes) by one lane with cp.async.bulk.tensor, completing on the warp's mbarrier for
 // that buffer; the pair walk is identical in every lane, so the tile coordinates are warp-uniform.
 // tph: the two buffers' mbarrier phase bits (carried across calls).
-template <int C, bool TRUNC, bool TMA = false>
-MPB_DEVI void engine(int ph, int NB, const Arr& AX, const Arr& AY, const Arr& DST, const Arr& T, const Arr& N,
-                     const Arr& OUT, uint32_t& orlo, uint32_t& tl1, const Stage& sg, uint32_t* tph = nullptr) {
+template <int C, bool TRUNC, bool TMA = false, class AR = Arr>
+MPB_DEVI void engine(int ph, int NB, const AR& AX, const AR& AY, const AR& DST, const AR& T, const AR& N,
+                     const AR& OUT, uint32_t& orlo, uint32_t& tl1, const Stage& sg, uint32_t* tph = nullptr) {
     uint32_t W[2 * C + 1];
     w_zero<C>(W);
     uint32_t carry = 0, borrow = 0;
@@ -290,13 +304,24 @@ MPB_DEVI void engine(int ph, int NB, const Arr& AX, const Arr& AY, const Arr& DS
             }
         } else {
             const uint32_t b = sg.base + (uint32_t)(buf * 2 * (C / 4)) * kStageCS;
-            const uint32_t cx = (uint32_t)ss * (C / 4), cy = (uint32_t)(kk - ss) * (C / 4);
+            if constexpr (AR::kSBC != 0) {  // warp tile: one address per block, immediate row offsets
+                const char* bx = reinterpret_cast<const char*>(AX.addr(ss * (C / 4)));
 #pragma unroll
-            for (int q = 0; q < C / 4; q++) cp_async16(b + q * kStageCS, chunk_addr(axp, cx + q, sbx));
-            if (!(sqr && 2 * ss == kk)) {
+                for (int q = 0; q < C / 4; q++) cp_async16(b + q * kStageCS, bx + q * AR::kSBC);
+                if (!(sqr && 2 * ss == kk)) {
+                    const char* by = reinterpret_cast<const char*>(AY.addr((kk - ss) * (C / 4)));
 #pragma unroll
-                for (int q = 0; q < C / 4; q++)
-                    cp_async16(b + (C / 4 + q) * kStageCS, chunk_addr(ayp, cy + q, sby));
+                    for (int q = 0; q < C / 4; q++) cp_async16(b + (C / 4 + q) * kStageCS, by + q * AR::kSBC);
+                }
+            } else {
+                const uint32_t cx = (uint32_t)ss * (C / 4), cy = (uint32_t)(kk - ss) * (C / 4);
+#pragma unroll
+                for (int q = 0; q < C / 4; q++) cp_async16(b + q * kStageCS, chunk_addr(axp, cx + q, sbx));
+                if (!(sqr && 2 * ss == kk)) {
+#pragma unroll
+                    for (int q = 0; q < C / 4; q++)
+                        cp_async16(b + (C / 4 + q) * kStageCS, chunk_addr(ayp, cy + q, sby));
+                }
             }
             cp_commit();
         }
@@ -433,16 +458,16 @@ MPB_DEVI void engine(int ph, int NB, const Arr& AX, const Arr& AY, const Arr& DS
 //   mode REDC: OUT = T*R^-1 mod N for the 2L-word T already in scratch T
 enum { MODE_MUL = 0, MODE_SQR = 1, MODE_REDC = 2 };
 
-template <int C, bool TRUNC, bool TMA = false>
-MPB_DEVI void mont_op(int mode, int NB, const Arr& X, const Arr& B, const Arr& N, const Arr& NP, const Arr& T, const Arr& Q,
-                      const Arr& OUT, const Stage& sg, uint32_t* tph = nullptr) {
+template <int C, bool TRUNC, bool TMA = false, class AR = Arr>
+MPB_DEVI void mont_op(int mode, int NB, const AR& X, const AR& B, const AR& N, const AR& NP, const AR& T, const AR& Q,
+                      const AR& OUT, const Stage& sg, uint32_t* tph = nullptr) {
     uint32_t orlo = 0, tl1 = 0;
 #pragma unroll 1
     for (int step = mode == MODE_REDC ? 1 : 0; step < 3; step++) {
         const int ph = step == 0 ? (mode == MODE_SQR ? PH_SQR : PH_MUL) : (step == 1 ? PH_Q : PH_HI);
-        const Arr ax = step == 0 ? X : (step == 1 ? T : Q);
-        const Arr ay = step == 0 ? B : (step == 1 ? NP : N);
-        const Arr dst = step == 0 ? T : Q;
+        const AR ax = step == 0 ? X : (step == 1 ? T : Q);
+        const AR ay = step == 0 ? B : (step == 1 ? NP : N);
+        const AR dst = step == 0 ? T : Q;
         engine<C, TRUNC, TMA>(ph, NB, ax, ay, dst, T, N, OUT, orlo, tl1, sg, tph);
     }
 }
@@ -456,9 +481,9 @@ MPB_DEVI void mont_op(int mode, int NB, const Arr& X, const Arr& B, const Arr& N
 // (block 0 of Z vanishes by the choice of m_i).  Y < 2N throughout, so Y has L limbs plus a top
 // bit; the result is canonicalised by one masked conditional subtraction.  B_ONE: B = 1 (used
 // for REDC(X) = MontMul(X, 1) in the exponentiation).  Scratch: Y (L limbs), M (C limbs).
-template <int C>
-MPB_DEVI void cios_op(int NB, const Arr& X, const Arr& B, bool b_one, const Arr& N, const Arr& NP, const Arr& Y,
-                      const Arr& M, const Arr& OUT) {
+template <int C, class AR = Arr>
+MPB_DEVI void cios_op(int NB, const AR& X, const AR& B, bool b_one, const AR& N, const AR& NP, const AR& Y,
+                      const AR& M, const AR& OUT) {
     uint32_t ytop = 0;
 #pragma unroll 1
     for (int i = 0; i < NB; i++) {
@@ -547,8 +572,8 @@ MPB_DEVI void cios_op(int NB, const Arr& X, const Arr& B, bool b_one, const Arr&
 // loads in flight per step; accumulators stay in registers at every L.
 // part / nparts: this thread scans chunk groups part, part + nparts, ... (cooperative operands
 // split the scan between their lanes; every entry is still read in full by the operand's lanes).
-template <int U>
-MPB_DEVI void ct_select(const Arr& G, int L, int nent, uint32_t idx, const Arr& OUT, int part = 0, int nparts = 1) {
+template <int U, class AR = Arr>
+MPB_DEVI void ct_select(const AR& G, int L, int nent, uint32_t idx, const AR& OUT, int part = 0, int nparts = 1) {
     const int Q4 = L / 4;
 
 #ifdef MPB_SEL_G

@@ -51,7 +51,9 @@ def test_host_only_helpers(lib):
     assert lib.mpb_supported(2048) == 1 and lib.mpb_supported(700) == 1 and lib.mpb_supported(20000) == 0
     lib.mont_batch_modexp_ct_workspace.restype = ctypes.c_size_t
     lib.mont_batch_modexp_ct_workspace.argtypes = [ctypes.c_size_t, ctypes.c_int, ctypes.c_int, ctypes.c_int]
-    assert lib.mont_batch_modexp_ct_workspace(10, 2048, 5, 0) == 10 * 64 * (32 + 5) * 4
+    # warp-tiled exponentiation workspace: count rounded up to 32 operands, 2^w + 7 arrays of L limbs
+    assert lib.mont_batch_modexp_ct_workspace(10, 2048, 5, 0) == 32 * 64 * (32 + 7) * 4
+    assert lib.mont_batch_modexp_ct_workspace(64, 2048, 5, 0) == 64 * 64 * (32 + 7) * 4
     assert lib.mont_batch_modexp_ct_workspace(10, 2048, 7, 0) == 0
     lib.mont_batch_setup_workspace.restype = ctypes.c_size_t
     lib.mont_batch_setup_workspace.argtypes = [ctypes.c_size_t, ctypes.c_int]
