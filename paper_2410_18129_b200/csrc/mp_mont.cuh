@@ -568,19 +568,13 @@ MPB_DEVI void cios_op(int NB, const AR& X, const AR& B, bool b_one, const AR& N,
 // ---------------------------------------------------------- CT table select
 // OUT = G[idx] by a masked scan of every entry ("constant-time batch selection").
 // Entry e, chunk q lives at chunk index e*(L/4) + q of G.  The scan is bound by DRAM latency
-// (the tables of all resident operands exceed L2), so it keeps SEL_U entries x SEL_G chunks of
+// (the tables of all resident operands exceed L2), so it keeps U entries x GRP chunks of
 // loads in flight per step; accumulators stay in registers at every L.
 // part / nparts: this thread scans chunk groups part, part + nparts, ... (cooperative operands
 // split the scan between their lanes; every entry is still read in full by the operand's lanes).
-template <int U, class AR = Arr>
+template <int U, int GRP, class AR = Arr>
 MPB_DEVI void ct_select(const AR& G, int L, int nent, uint32_t idx, const AR& OUT, int part = 0, int nparts = 1) {
     const int Q4 = L / 4;
-
-#ifdef MPB_SEL_G
-    constexpr int GRP = MPB_SEL_G;
-#else
-    constexpr int GRP = 4;
-#endif
 #pragma unroll 1
     for (int g0 = part * GRP; g0 < Q4; g0 += nparts * GRP) {
         uint4 acc[GRP];
