@@ -43,15 +43,15 @@ __host__ __device__ constexpr int select_unroll() {
     return 4;
 #endif
 }
-// chunks per entry loaded per step of the table scan (x select_unroll entries in flight: 32 loads
-// at C >= 12, measured +0.6 % over 16 at L = 64; the C < 12 kernels have 102 registers and the
-// cooperative kernel keeps 16, its lanes splitting the groups)
-template <int C>
+// chunks per entry loaded per step of the table scan (x select_unroll entries in flight): 32 loads
+// in the tiled C = 16 kernels (+0.6 % over 16 at L = 64); 16 elsewhere (the C < 12 kernels have 102
+// registers, the generic-NB ones spill with 32, the cooperative lanes split the groups)
+template <int C, bool TILE>
 __host__ __device__ constexpr int select_group() {
 #ifdef MPB_SEL_G
     return MPB_SEL_G;
 #else
-    return C >= 12 ? 8 : 4;
+    return C == 16 && TILE ? 8 : 4;
 #endif
 }
 // dynamic shared memory: 2 buffers x 2 operand blocks x C/4 chunks of 16 bytes per thread (as
@@ -159,7 +159,8 @@ __global__ void __launch_bounds__(kThreads) k_mont_redc(const uint32_t* __restri
 //   then per window j = W-2 .. 0:  w x Y = MontSqr(Y),  S = CTsel(G, window j)
 //                                  (P:L765-766),  Y = MontMul(Y, S)
 //   last op          out = REDC(Y)
-// workspace: TILE (schoolbook products, cp.async staging -- the default path): warp-tiled arrays
+// workspace: TILE (compile-time block count, schoolbook products, cp.async staging -- the hot
+// sizes): warp-tiled arrays
 // (ArrT, DESIGN 5.6) over cpad = count rounded up to 32 operands:
 //   G (2^w * L) | Y (L) | T (2L) | Q (L) | S (L) | N (L) | N' (L)
 // with N, N', base and R^2 copied in from the word-sliced inputs and the result copied out, so
@@ -168,7 +169,14 @@ __global__ void __launch_bounds__(kThreads) k_mont_redc(const uint32_t* __restri
 // (kara_scratch_blocks(nb, KLEV) blocks; KLEV = algo levels for the products).
 // The whole exponentiation of operand k (of `count`, the arrays' stride).  COOP: two lanes per
 // operand (mp_coop.cuh), role = lane & 1, mask = the active pairs of the warp.
-__host__ __device__ constexpr bool modexp_tiled(int KLEV, bool TMA) { return KLEV == 0 && !TMA; }
+#ifndef MPB_TILE
+#define MPB_TILE 1
+#endif
+// tiled for the compile-time block counts (the hot sizes); the generic-NB kernels run measurably
+// slower with it (1536 / 2560 / 4108 bits: 5-20 %) and keep the word-sliced workspace
+__host__ __device__ constexpr bool modexp_tiled(int KLEV, bool TMA, int NBT) {
+    return MPB_TILE && KLEV == 0 && !TMA && NBT != 0;
+}
 // warp-tiled view of operand k in an array of nch chunks per operand
 MPB_DEVI ArrT tarr(uint32_t* base, int nch, size_t k) {
     char* p = reinterpret_cast<char*>(base) + (k >> 5) * ((size_t)nch * kTileSB) + (k & 31) * 16;
@@ -178,7 +186,7 @@ template <int C, int RM, int NBT, int KLEV, bool COOP, bool TMA = false>
 MPB_DEVI void modexp_body(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
                           const uint32_t* exp, uint32_t* out, size_t count, size_t k, int nb_rt, int bits, int w,
                           uint32_t* ws, uint32_t role, unsigned mask, const TmaMaps* maps = nullptr) {
-    constexpr bool TILE = modexp_tiled(KLEV, TMA);
+    constexpr bool TILE = modexp_tiled(KLEV, TMA, NBT);
     using A = std::conditional_t<TILE, ArrT, Arr>;
     const int nb = NBT ? NBT : nb_rt;  // compile-time block count for the hot sizes
     const int L = C * nb, Q4 = L / 4;
@@ -281,7 +289,7 @@ MPB_DEVI void modexp_body(const uint32_t* N, const uint32_t* NP, const uint32_t*
                 ct_select<select_unroll<C>(), 4>(G, L, nent, v & ((1u << w) - 1u), O, (int)role, 2);
                 __syncwarp(mask);
             } else {
-                ct_select<select_unroll<C>(), select_group<C>()>(G, L, nent, v & ((1u << w) - 1u), O);
+                ct_select<select_unroll<C>(), select_group<C, TILE>()>(G, L, nent, v & ((1u << w) - 1u), O);
             }
             continue;
         }
