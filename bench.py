@@ -72,9 +72,9 @@ def modexp_imad(bits: int, w: int, redc: int) -> int:
 
 def ncu_traffic():
     """dram__bytes_read.sum + dram__bytes_write.sum per k_modexp launch (TB), from the committed
-    `ncu --set full` capture of this exact launch (profiles/r01_v5_ncu_modexp.json), else None."""
+    `ncu --set full` capture of this exact launch (profiles/r01_v6_ncu_modexp.json), else None."""
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "r01_v5_ncu_modexp.json")))
+        d = json.load(open(os.path.join(ROOT, "profiles", "r01_v6_ncu_modexp.json")))
         if d.get("operands_per_launch") == COUNT:
             return d["dram_bytes_per_launch"] / 1e12
     except Exception:
@@ -281,7 +281,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic", "config": config_dict(world),
             "roofline": {
-                "bound": "alu", "kernel": "k_modexp<16,4,true>",
+                "bound": "alu", "kernel": "k_modexp<C=16, truncated REDC, NB=4, schoolbook>",
                 "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TIMAD/s", "frac": achieved / peak,
                 "traffic_unit": "TB per launch (DRAM, ncu; algorithmic table-scan bytes 0.88 TB)",
                 "traffic": ncu_traffic(),
