@@ -566,6 +566,11 @@ MPB_DEVI void cios_op(int NB, const AR& X, const AR& B, bool b_one, const AR& N,
 }
 
 // ---------------------------------------------------------- CT table select
+#ifdef MPB_PLANTED_BRANCH
+#define MPB_PLANTED 1
+#else
+#define MPB_PLANTED 0
+#endif
 // OUT = G[idx] by a masked scan of every entry ("constant-time batch selection").
 // Entry e, chunk q lives at chunk index e*(L/4) + q of G.  The scan is bound by DRAM latency
 // (the tables of all resident operands exceed L2), so it keeps U entries x GRP chunks of
@@ -575,6 +580,44 @@ MPB_DEVI void cios_op(int NB, const AR& X, const AR& B, bool b_one, const AR& N,
 template <int U, int GRP, class AR = Arr>
 MPB_DEVI void ct_select(const AR& G, int L, int nent, uint32_t idx, const AR& OUT, int part = 0, int nparts = 1) {
     const int Q4 = L / 4;
+    if constexpr (AR::kSBC != 0) {
+        // warp tile: every load of a step is an immediate offset from one address, and with whole
+        // steps (nent % U == 0, Q4 % GRP == 0: the tiled sizes at w >= 2) no load needs a guard
+        if (!MPB_PLANTED && nent % U == 0 && Q4 % GRP == 0) {
+            constexpr int RW = AR::kSBC / 16;  // uint4 per chunk row
+#pragma unroll 1
+            for (int g0 = part * GRP; g0 < Q4; g0 += nparts * GRP) {
+                uint4 acc[GRP];
+#pragma unroll
+                for (int q = 0; q < GRP; q++) acc[q] = make_uint4(0, 0, 0, 0);
+#pragma unroll 1
+                for (int e0 = 0; e0 < nent; e0 += U) {
+                    const uint4* eb = G.addr(e0 * Q4 + g0);
+                    uint4 v[U][GRP];
+#pragma unroll
+                    for (int u = 0; u < U; u++)
+#pragma unroll
+                        for (int q = 0; q < GRP; q++) v[u][q] = __ldcs(eb + (u * Q4 + q) * RW);
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        const uint32_t x = (uint32_t)(e0 + u) ^ idx;
+                        const uint32_t m = 0u - ((x - 1u) >> 31);  // all ones iff e == idx
+#pragma unroll
+                        for (int q = 0; q < GRP; q++) {
+                            acc[q].x |= v[u][q].x & m;
+                            acc[q].y |= v[u][q].y & m;
+                            acc[q].z |= v[u][q].z & m;
+                            acc[q].w |= v[u][q].w & m;
+                        }
+                    }
+                }
+                uint4* ob = OUT.addr(g0);
+#pragma unroll
+                for (int q = 0; q < GRP; q++) ob[q * RW] = acc[q];
+            }
+            return;
+        }
+    }
 #pragma unroll 1
     for (int g0 = part * GRP; g0 < Q4; g0 += nparts * GRP) {
         uint4 acc[GRP];
