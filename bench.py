@@ -72,9 +72,9 @@ def modexp_imad(bits: int, w: int, redc: int) -> int:
 
 def ncu_traffic():
     """dram__bytes_read.sum + dram__bytes_write.sum per k_modexp launch (TB), from the committed
-    `ncu --set full` capture of this exact launch (profiles/r01_v6_ncu_modexp.json), else None."""
+    `ncu --set full` capture of this exact launch (profiles/r01_v7_ncu_modexp.json), else None."""
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "r01_v6_ncu_modexp.json")))
+        d = json.load(open(os.path.join(ROOT, "profiles", "r01_v7_ncu_modexp.json")))
         if d.get("operands_per_launch") == COUNT:
             return d["dram_bytes_per_launch"] / 1e12
     except Exception:
