@@ -178,6 +178,24 @@ def test_modexp_window_independence(mpb, window):
     assert np.array_equal(out, O.batch_modexp(base, exp, bits, N))
 
 
+@pytest.mark.parametrize("bits", [2048, 3072])
+@pytest.mark.parametrize("count", [31, 32, 33, 65])
+def test_modexp_warp_tile_edges(mpb, bits, count):
+    """The exponentiation's warp-tiled workspace (DESIGN 5.6): counts around whole 32-operand tiles
+    (a ragged last tile, exactly one tile, one operand into the next), all REDC modes, windows on
+    the unguarded (w = 5) and guarded (w = 1) table-scan paths; first, last and a middle operand
+    against the oracle."""
+    N, base, exp = I.modexp_inputs(config=3, count=count, bits=bits, dataset=count)
+    dN = mpb.to_device(N)
+    Np, R2 = mpb.mont_batch_setup(dN, bits)
+    idx = [0, count // 2, count - 1]
+    for redc in REDC:
+        for w in (5, 1):
+            out = mpb.to_host(mpb.mont_batch_modexp_ct(dN, Np, R2, mpb.to_device(base), mpb.to_device(exp), bits,
+                                                       window=w, redc=redc))
+            assert np.array_equal(out[idx], O.batch_modexp(base[idx], exp[idx], bits, N[idx])), (redc, w)
+
+
 def test_modexp_special_exponents_and_bases(mpb):
     bits = 1024
     L = I.limbs_for_bits(bits)
