@@ -89,7 +89,7 @@ size_t mont_batch_workspace(size_t count, int bits);
  * squarings, a masked full-table scan and one Montgomery multiplication.
  * exp has L limbs and `bits` significant bits (zero padded); timing depends on
  * (count, bits, window, redc) only.  window in 1..6.  exp = 0 gives 1 (0^0 = 1).
- * For >= 3072-bit operands, batches below a quarter of the device's resident capacity run with
+ * For >= 3072-bit operands, batches of at most (SM count x 64) operands run with
  * two lanes per operand (the result is the same; only the schedule differs). */
 int mont_batch_modexp_ct(const uint32_t* N, const uint32_t* Nprime, const uint32_t* R2, const uint32_t* base,
                          const uint32_t* exp, uint32_t* out, size_t count, int bits, int window, int redc,

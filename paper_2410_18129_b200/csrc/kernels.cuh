@@ -344,8 +344,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_modexp_tma(
                                             0xFFFFFFFFu, &maps);
 }
 
-// Two lanes per operand (mp_coop.cuh): for >= 3072-bit batches below a quarter of the resident
-// capacity (Launch::modexp).
+// Two lanes per operand (mp_coop.cuh): for >= 3072-bit batches whose cooperative launch fits one
+// CTA per SM (Launch::modexp).
 template <int C, int RM, int NBT>
 __global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_modexp_coop(
     const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP, const uint32_t* __restrict__ R2,
@@ -705,11 +705,12 @@ void Launch<C>::modexp(const uint32_t* N, const uint32_t* NP, const uint32_t* R2
         // Measured: two lanes per operand pay for >= 3072-bit operands at low
         // occupancy (1.23x at 4096 bits); at 1024/2048 bits or near half occupancy they do not.
         if (C * nb < 96) return single(0, count);
-        int dev = 0, sms = 148, per_sm = min_blocks<C>();
+        int dev = 0, sms = 148;
         if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_modexp<C, 1, NBT, 0>, kThreads, sm);
-        const size_t slots = (size_t)sms * (size_t)(per_sm > 0 ? per_sm : 1) * kThreads;
-        if (4 * count <= slots) return coop(0, count);  // small batch
+        // small batch: the cooperative launch still fits one CTA per SM (measured crossover: two
+        // lanes per operand win 1.19x at 4096 bits up to 9472 operands = 148 CTAs, and lose once
+        // SMs hold two cooperative CTAs, e.g. 638 vs 607 ms at 14208)
+        if (2 * count <= (size_t)sms * kThreads) return coop(0, count);
         // (a cooperative tail after the whole waves measured neutral at 2^16 x 4096 bits: the
         // one-thread tail already overlaps the drain of the last wave)
         single(0, count);

@@ -2,7 +2,7 @@
 //
 // The one-thread-per-operand engine (mp_mont.cuh) needs one resident thread per operand, so a
 // batch much smaller than the resident capacity leaves SMs idle (used for >= 3072-bit batches
-// below a quarter of the capacity: 1.25x at 4096 bits).  Here the two lanes 2m, 2m+1 of a warp own operand m (role r = lane & 1) and split the
+// whose cooperative launch fits one CTA per SM: 1.19x at 4096 bits).  Here the two lanes 2m, 2m+1 of a warp own operand m (role r = lane & 1) and split the
 // block products of every block column between them: in iteration i of column k, role r takes
 // the pair s = s_lo + 2i + r (PH_SQR: the off-diagonal pairs, then one iteration for the diagonal
 // block, which role 0 computes and role 1 runs on a zero block).  A role without a pair in an
