@@ -191,7 +191,7 @@ def config_dict(world: int) -> dict:
                         "full-length exponents)",
             "bits": BITS, "window": WINDOW, "redc": "truncated", "count_per_gpu": COUNT,
             "global_batch": COUNT * world, "parallelism": f"independent slices x{world}",
-            "l2": "no flush: per-step working set (inputs 320 MiB + tables/scratch 2.4 GiB) > 126 MB L2"}
+            "l2": "no flush: per-step working set (inputs 320 MiB + tables/scratch 2.5 GiB) > 126 MB L2"}
 
 
 # ------------------------------------------------------------------- ours
