@@ -159,14 +159,13 @@ __global__ void __launch_bounds__(kThreads) k_mont_redc(const uint32_t* __restri
 //   then per window j = W-2 .. 0:  w x Y = MontSqr(Y),  S = CTsel(G, window j)
 //                                  (P:L765-766),  Y = MontMul(Y, S)
 //   last op          out = REDC(Y)
-// workspace: TILE (compile-time block count, schoolbook products, cp.async staging -- the hot
-// sizes): warp-tiled arrays
-// (ArrT, DESIGN 5.6) over cpad = count rounded up to 32 operands:
+// workspace: TILE (compile-time block count, schoolbook products, cp.async staging: the hot
+// sizes) -- warp-tiled arrays (ArrT, DESIGN 5.6) over cpad = count rounded up to 32 operands:
 //   G (2^w * L) | Y (L) | T (2L) | Q (L) | S (L) | N (L) | N' (L)
 // with N, N', base and R^2 copied in from the word-sliced inputs and the result copied out, so
-// every engine array has the compile-time chunk stride.  Otherwise (Karatsuba products, TMA
-// tiles): word-sliced arrays, stride count: G | Y | T | Q | S | Karatsuba scratch
-// (kara_scratch_blocks(nb, KLEV) blocks; KLEV = algo levels for the products).
+// every engine array has the compile-time chunk stride.  Otherwise (generic block count,
+// Karatsuba products, TMA tiles) -- word-sliced arrays, stride count: G | Y | T | Q | S |
+// Karatsuba scratch (kara_scratch_blocks(nb, KLEV) blocks; KLEV = algo levels for the products).
 // The whole exponentiation of operand k (of `count`, the arrays' stride).  COOP: two lanes per
 // operand (mp_coop.cuh), role = lane & 1, mask = the active pairs of the warp.
 #ifndef MPB_TILE
