@@ -8,10 +8,14 @@ exit REDC all inside one kernel).  Inputs are resident in HBM before timing star
 per-step working set (inputs 320 MiB + window tables and scratch 2.4 GiB) is larger than
 the 126 MB L2, so no explicit flush is needed between steps.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload config3|config5]
 
-N > 1 runs under torchrun, one rank per GPU: each rank takes its own 2^18 slice
-(independent units, no data-path collective; weak scaling), timing is the max over ranks.
+N > 1: one rank per GPU, under torchrun or -- when WORLD_SIZE is unset -- started here by
+torch.multiprocessing (launcher.spawn); NCCL only for the barrier and the max over ranks.
+Default (config3): each rank takes its own 2^18 batch (independent units, no data-path
+collective; weak scaling).  --workload config5: one 2^22 batch split into contiguous slices
+(strong scaling), with the oracle check of a seeded 4096-element subset and a slicing-independent
+digest of all outputs in the line (G-invariance across runs with 1/2/4/8 GPUs).
 `--impl reference` times the plain CPU oracle (oracle/, test infrastructure) on the host
 cores on bounded samples of the same workload -- the reference arm of this tier.
 Prints ONE JSON line on rank 0.
@@ -37,7 +41,9 @@ BASELINE = json.load(open(os.path.join(ROOT, "BASELINE.json")))
 METRIC = BASELINE["metric"]
 UNIT = "modexp/s"
 BITS, WINDOW, COUNT, CONFIG = 2048, 5, 1 << 18, 3
+COUNT5 = 1 << 22  # config 5: whole-box batch
 SMS, IMAD_PER_CLK_SM = 148, 64  # K0-measured 63.6 (profiles/r01_microbench_int.json)
+K0_PRODUCTS_PER_CLK_SM = 31.1  # measured fused IMAD.WIDE.U32.X chain rate (profiles/r01_microbench_int.json)
 
 
 # ------------------------------------------------------------------ roofline
@@ -70,16 +76,23 @@ def modexp_imad(bits: int, w: int, redc: int) -> int:
     return (W - 1) * w * c["sqr"] + ((W - 1) + (1 << w) - 1) * c["mul"] + 2 * c["redc"]
 
 
+NCU_CAPTURE = "r02_ncu_modexp.json"  # the committed `ncu --set full` summary of this launch
+
+
 def ncu_traffic():
-    """dram__bytes_read.sum + dram__bytes_write.sum per k_modexp launch (TB), from the committed
-    `ncu --set full` capture of this exact launch (profiles/r01_v7_ncu_modexp.json), else None."""
-    try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "r01_v7_ncu_modexp.json")))
-        if d.get("operands_per_launch") == COUNT:
-            return d["dram_bytes_per_launch"] / 1e12
-    except Exception:
-        pass
-    return None
+    """(TB per launch, note): dram__bytes_read.sum + dram__bytes_write.sum of k_modexp from the
+    committed `ncu --set full` capture of this same launch (a timed run cannot be profiled), or
+    (None, note) when no capture of this launch shape is committed."""
+    for name in (NCU_CAPTURE, "r01_v7_ncu_modexp.json"):
+        try:
+            d = json.load(open(os.path.join(ROOT, "profiles", name)))
+            if d.get("operands_per_launch") == COUNT:
+                return d["dram_bytes_per_launch"] / 1e12, (
+                    f"from profiles/{name} (ncu --set full of this launch shape, NOT measured in this run); "
+                    f"algorithmic table-scan bytes 0.881 TB per launch")
+        except Exception:
+            pass
+    return None, "no committed ncu capture of this launch"
 
 
 # -------------------------------------------------------------------- clocks
@@ -185,7 +198,15 @@ def run_reference(args, rank: int, world: int) -> None:
     print(json.dumps(line), flush=True)
 
 
-def config_dict(world: int) -> dict:
+def config_dict(world: int, c5: bool = False) -> dict:
+    if c5:
+        return {"workload": "BASELINE config 5: one 2^22-operand batch of 2048-bit constant-time fixed-window "
+                            "modexps (window 5, truncated REDC) split into contiguous slices across the GPUs "
+                            "(random odd moduli with top bit set, bases in [0,N), full-length exponents; "
+                            "chunk-seeded so every slicing sees the same operands)",
+                "bits": BITS, "window": WINDOW, "redc": "truncated", "count_per_gpu": COUNT5 // world,
+                "global_batch": COUNT5, "parallelism": f"independent slices x{world}",
+                "l2": "no flush: per-step working set (inputs >= 640 MiB + tables/scratch >= 5 GiB) > 126 MB L2"}
     return {"workload": "BASELINE config 3: 2048-bit constant-time fixed-window modexp, window 5, truncated "
                         "REDC, batch 2^18 per GPU (random odd moduli with top bit set, bases in [0,N), "
                         "full-length exponents)",
@@ -195,29 +216,36 @@ def config_dict(world: int) -> dict:
 
 
 # ------------------------------------------------------------------- ours
-def run_ours(args, rank: int, world: int, local_rank: int) -> None:
+def run_ours(args) -> None:
     import torch
 
-    from paper_2410_18129_b200 import mpb
+    from paper_2410_18129_b200 import mpb, shard
+    from paper_2410_18129_b200.launcher import Ranks
 
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
     torch.cuda.set_device(local_rank)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    rk = Ranks("nccl", device=torch.device("cuda", local_rank))
+    rank, world = rk.rank, rk.world
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: {world} rank(s) running but --gpus {args.gpus}")
+    c5 = args.workload == "config5"
+    L = I.limbs_for_bits(BITS)
+    if c5:  # strong scaling: one global 2^22 batch, contiguous slices (shard.plan)
+        a0, b0 = shard.rank_slice(COUNT5, rank, world)
+        N, base, exp = I.modexp_inputs_range(5, a0, b0, BITS)
+    else:  # weak scaling: 2^18 operands per rank (dataset = rank)
+        a0, b0 = 0, COUNT
+        N, base, exp = I.modexp_inputs(config=CONFIG, count=COUNT, bits=BITS, dataset=rank)
+    count = b0 - a0
 
     def barrier():
-        if dist:
-            dist.barrier()
+        rk.barrier()
         torch.cuda.synchronize()
 
-    L = I.limbs_for_bits(BITS)
-    N, base, exp = I.modexp_inputs(config=CONFIG, count=COUNT, bits=BITS, dataset=rank)
     dN, dB, dE = (mpb.to_device(x) for x in (N, base, exp))
     Np, R2 = mpb.mont_batch_setup(dN, BITS)
-    ws = mpb.modexp_workspace(COUNT, BITS, WINDOW)
-    out = mpb.empty_sliced(L, COUNT)
+    ws = mpb.modexp_workspace(count, BITS, WINDOW)
+    out = mpb.empty_sliced(L, count)
     stream = torch.cuda.current_stream()
 
     def step():
@@ -234,75 +262,94 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
             ev[i + 1].record(stream)
         barrier()
     per_launch_ms = [ev[i].elapsed_time(ev[i + 1]) for i in range(args.steps)]
-    total_ms = ev[0].elapsed_time(ev[-1])
-    t = torch.tensor([total_ms], device="cuda")
-    if dist:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    total_ms = rk.max(ev[0].elapsed_time(ev[-1]))  # the slowest rank's device time
+    dev_out = mpb.to_host(out)
 
     # end to end through the public host-buffer call (pinned host memory, H2D + setup + modexp + D2H)
     e2e_steps = max(1, min(args.steps, 3))
     hN, hB, hE = (torch.from_numpy(x.view(np.int32)).pin_memory() for x in (N, base, exp))
     hO = torch.empty_like(hN).pin_memory()
-    import ctypes
-
-    lib = mpb._lib
 
     def e2e_call():
-        rc = lib.mpb_modexp_host(hN.data_ptr(), hB.data_ptr(), hE.data_ptr(), hO.data_ptr(), COUNT, BITS, WINDOW,
-                                 mpb.REDC_TRUNCATED, ctypes.c_void_p(stream.cuda_stream))
-        if rc != 0:
-            raise RuntimeError(lib.mpb_last_error().decode())
+        mpb.modexp_host_ptrs(hN.data_ptr(), hB.data_ptr(), hE.data_ptr(), hO.data_ptr(), count, BITS, WINDOW,
+                             mpb.REDC_TRUNCATED, stream.cuda_stream)
 
-    e2e_call()  # warm-up: the first call sizes the stream-ordered memory pool
+    e2e_call()  # warm-up: the first call sizes the library's memory pool
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         e2e_call()
     barrier()
-    e2e_s = time.perf_counter() - t0
-    te = torch.tensor([e2e_s], device="cuda")
-    if dist:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_s = float(te.item())
-    ok_e2e = np.array_equal(hO.numpy().view(np.uint32)[:4], mpb.to_host(out)[:4])
+    e2e_s = rk.max(time.perf_counter() - t0)
+    ok_e2e = rk.sum(0 if np.array_equal(hO.numpy().view(np.uint32), dev_out) else 1) == 0
+
+    extra = {}
+    if c5:  # parity on the seeded 4096-element subset of the global batch + G-invariant digest
+        import oracle as O
+
+        sub = np.sort(np.random.default_rng(5).choice(COUNT5, size=4096, replace=False))
+        mine = sub[(sub >= a0) & (sub < b0)] - a0
+        cores = max(1, (os.cpu_count() or 1) // world)
+        bad = 0
+        if len(mine):
+            ref = O.batch_modexp(base[mine], exp[mine], BITS, N[mine], threads=cores)
+            bad = int((ref != dev_out[mine]).any(axis=1).sum())
+        bad = rk.sum(bad)
+        dig = shard.digest_combine(rk.gather_objects(shard.digest_part(dev_out, a0)))
+        extra = {"oracle_subset": {"checked": 4096, "mismatches": bad, "seed": 5},
+                 "digest": dig, "g_invariant_digest_of": f"all {COUNT5} outputs in global order"}
 
     if rank == 0:
         ms = total_ms / args.steps
-        value = world * COUNT / (ms / 1000.0)
+        total = COUNT5 if c5 else world * COUNT
+        value = total / (ms / 1000.0)
         kern_ms = float(np.mean(per_launch_ms))
-        imad = modexp_imad(BITS, WINDOW, True) * COUNT
+        imad = modexp_imad(BITS, WINDOW, True) * count
         clk = clocks.summary()
         f_max = (clk["sm_max_mhz"] or 1965) * 1e6
         peak = SMS * IMAD_PER_CLK_SM * f_max
+        peak_k0 = SMS * 2 * K0_PRODUCTS_PER_CLK_SM * f_max
         achieved = imad / (kern_ms / 1000.0)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u32", "data": "synthetic", "config": config_dict(world),
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if c5 else "weak",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic", "config": config_dict(world, c5),
             "roofline": {
-                "bound": "alu", "kernel": "k_modexp<C=16, truncated REDC, NB=4, schoolbook>",
+                "bound": "imad", "pipe": "fmaheavy (IMAD.WIDE.U32.X: one fused 32x32->64 product = 2 IMAD)",
+                "kernel": "k_modexp<C=16, truncated REDC, NB=4, schoolbook>",
                 "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TIMAD/s", "frac": achieved / peak,
-                "traffic_unit": "TB per launch (DRAM, ncu; algorithmic table-scan bytes 0.88 TB)",
-                "traffic": ncu_traffic(),
-                "peak_basis": f"{SMS} SMs x {IMAD_PER_CLK_SM} IMAD/clk/SM (K0 measured 63.6) x {f_max/1e6:.0f} MHz",
+                "peak_basis": f"nominal: {SMS} SMs x {IMAD_PER_CLK_SM} IMAD/clk/SM x {f_max/1e6:.0f} MHz "
+                              "(MEASURED_PEAKS.json has no integer peak; the profiling guide gives no integer fallback)",
+                "peak_k0": peak_k0 / 1e12, "frac_k0": achieved / peak_k0,
+                "peak_k0_basis": f"measured fused-chain rate {K0_PRODUCTS_PER_CLK_SM} products/clk/SM "
+                                 "(profiles/r01_microbench_int.json) x 2 IMAD x SMs x clock",
                 "frac_at_sampled_clock": (achieved / (SMS * IMAD_PER_CLK_SM * clk["sm_mhz"] * 1e6)
                                           if clk["sm_mhz"] else None),
                 "imad_per_modexp": modexp_imad(BITS, WINDOW, True),
+                "traffic": ncu_traffic()[0], "traffic_unit": "TB per launch",
+                "traffic_source": ncu_traffic()[1],
             },
             "clocks": clk,
-            "e2e": {"value": world * COUNT * e2e_steps / e2e_s, "unit": UNIT,
-                    "h2d_bytes_per_step": 3 * COUNT * L * 4, "d2h_bytes_per_step": COUNT * L * 4,
+            "e2e": {"value": total * e2e_steps / e2e_s, "unit": UNIT,
+                    "h2d_bytes_per_step": 3 * total * L * 4, "d2h_bytes_per_step": total * L * 4,
                     "includes": "pinned H2D of N/base/exp, layout expand, mont_batch_setup, modexp, contract, D2H",
                     "matches_device_result": bool(ok_e2e)},
             "gpu_launches": args.steps,
             "kernel_ms": {"mean": kern_ms, "min": float(np.min(per_launch_ms)), "max": float(np.max(per_launch_ms))},
+            **extra,
         }
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_oracle_sample()
         print(json.dumps(line), flush=True)
-    if dist:
-        dist.destroy_process_group()
+    rk.close()
+
+
+def _rank_main(args) -> None:
+    if args.impl == "reference":
+        run_reference(args, int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", args.gpus)))
+    else:
+        run_ours(args)
 
 
 def main():
@@ -311,15 +358,25 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="config3", choices=["config3", "config5"],
+                    help="config3: 2^18 operands per GPU (weak scaling, the default); config5: one 2^22 batch "
+                         "split across the GPUs (strong scaling), oracle subset + G-invariant digest")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
-    rank = int(os.environ.get("RANK", 0))
-    world = int(os.environ.get("WORLD_SIZE", args.gpus if args.impl == "reference" else 1))
-    local_rank = int(os.environ.get("LOCAL_RANK", 0))
-    if args.impl == "reference":
-        run_reference(args, rank, world)
-    else:
-        run_ours(args, rank, world, local_rank)
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # started as `python bench.py --gpus N` without torchrun: start the N ranks here
+        import torch
+
+        from paper_2410_18129_b200.launcher import spawn
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            raise SystemExit(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible")
+        spawn(args.gpus, _rank_main, args)
+        return
+    _rank_main(args)
 
 
 if __name__ == "__main__":

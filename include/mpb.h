@@ -47,7 +47,9 @@ typedef enum { MPB_OK = 0, MPB_EINVAL = -1, MPB_EUNSUPPORTED = -2, MPB_ECUDA = -
  * Nprime).  CIOS applies to mont_batch_mul/sqr and the exponentiation (schoolbook only), not
  * to a stand-alone mont_batch_redc (MPB_EUNSUPPORTED). */
 enum { MPB_REDC_FULL = 0, MPB_REDC_TRUNCATED = 1, MPB_REDC_CIOS = 2 };
-/* AUTO = the measured crossover; KARATSUBA = one level, KARATSUBA2 = two levels. */
+/* AUTO = schoolbook: on sm_100a the blocked schoolbook engine beat every Karatsuba variant at every
+ * measured size, so there is no crossover to select; KARATSUBA = one level,
+ * KARATSUBA2 = two levels, explicit requests only. */
 enum { MPB_ALGO_AUTO = 0, MPB_ALGO_SCHOOLBOOK = 1, MPB_ALGO_KARATSUBA = 2, MPB_ALGO_KARATSUBA2 = 3 };
 
 /* L(bits) = 4*ceil(bits/128); 0 if bits <= 0. */
@@ -78,7 +80,10 @@ int mont_batch_mul(const uint32_t* a, const uint32_t* b, const uint32_t* N, cons
 /* c = a^2*R^-1 mod N (canonical). */
 int mont_batch_sqr(const uint32_t* a, const uint32_t* N, const uint32_t* Nprime, uint32_t* c, size_t count,
                    int bits, int redc, void* workspace, size_t workspace_bytes, void* stream);
-/* c = T*R^-1 mod N for T < N*R given with 2L limbs (word-sliced with 2L limbs).  alg:montred. */
+/* c = T*R^-1 mod N for T < N*R given with 2L limbs (word-sliced with 2L limbs).  alg:montred.
+ * At 1024/2048/3072/4096/4108 bits this runs the exponentiation's own engine instantiation
+ * (compile-time block count, warp-tiled workspace), so it exercises the code mont_batch_modexp_ct
+ * ships.  workspace: mont_batch_workspace(count, bits) bytes. */
 int mont_batch_redc(const uint32_t* T, const uint32_t* N, const uint32_t* Nprime, uint32_t* c, size_t count,
                     int bits, int redc, void* workspace, size_t workspace_bytes, void* stream);
 size_t mont_batch_workspace(size_t count, int bits);
@@ -96,7 +101,10 @@ int mont_batch_modexp_ct(const uint32_t* N, const uint32_t* Nprime, const uint32
                          int algo, void* workspace, size_t workspace_bytes, void* stream);
 size_t mont_batch_modexp_ct_workspace(size_t count, int bits, int window, int algo);
 
-/* Montgomery constants: Nprime = (-N)^-1 mod R, R2 = R^2 mod N ("precomputed values"). */
+/* Montgomery constants: Nprime = (-N)^-1 mod R, R2 = R^2 mod N ("precomputed values").
+ * The schedule (number of modular doublings) depends on each modulus's bit length, read from its
+ * top limbs: moduli are public here.  (rsa_batch_crt_ct, whose primes are secret, runs the same
+ * kernel with the public length bits/2 instead.) */
 int mont_batch_setup(const uint32_t* N, uint32_t* Nprime, uint32_t* R2, size_t count, int bits,
                      void* workspace, size_t workspace_bytes, void* stream);
 size_t mont_batch_setup_workspace(size_t count, int bits);
@@ -107,7 +115,9 @@ size_t mont_batch_setup_workspace(size_t count, int bits);
  * m = m_q + q * (qinv * (m_p - m_q) mod p).  bits = modulus size (even, >= 128); c and m have
  * mpb_limbs(bits) limbs, p, q, dp, dq, qinv have mpb_limbs(bits/2) limbs (word-sliced, `count`
  * operands each).  Preconditions (not checked on the device): p, q odd with exactly bits/2 bits,
- * qinv = q^-1 mod p, c < p*q, dp, dq < 2^(bits/2).  redc selects the REDC mode of the
+ * qinv = q^-1 mod p, c < p*q, dp, dq < 2^(bits/2).  The Montgomery setup of p and q uses the public
+ * length bits/2, never one read from the primes; a prime of any other length violates the
+ * precondition and gives a wrong result (and Garner's single masked subtraction assumes q < 2p).  redc selects the REDC mode of the
  * exponentiation.  workspace: rsa_batch_crt_workspace(count, bits, window) bytes.
  * MPB_EUNSUPPORTED for count > 2^26 (the half-size exponentiation runs 2*count operands). */
 int rsa_batch_crt_ct(const uint32_t* c, const uint32_t* p, const uint32_t* q, const uint32_t* dp, const uint32_t* dq,
@@ -116,9 +126,11 @@ int rsa_batch_crt_ct(const uint32_t* c, const uint32_t* p, const uint32_t* q, co
 size_t rsa_batch_crt_workspace(size_t count, int bits, int window);
 
 /* End-to-end convenience over HOST buffers (operand-major, L limbs each; exp L limbs):
- * allocates device memory (stream-ordered, from the device's default memory pool, whose
- * release threshold it raises so that repeated calls reuse the allocation), copies in, runs
- * setup + modexp, copies out, synchronises.  Returns MPB_OK or an error; blocking. */
+ * allocates device memory (stream-ordered, from the library's OWN per-device memory pool, created
+ * on first use and kept with an unlimited release threshold so repeated calls reuse the
+ * allocation; the device's default pool is not touched), copies in, runs setup + modexp, copies
+ * out, synchronises.  Returns MPB_OK or an error; blocking.  Host buffers should be pinned for
+ * the copies to be asynchronous. */
 int mpb_modexp_host(const uint32_t* N, const uint32_t* base, const uint32_t* exp, uint32_t* out, size_t count,
                     int bits, int window, int redc, void* stream);
 

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "../../include/mpb.h"
@@ -96,6 +97,30 @@ int check_launch() {
 
 unsigned grid_for(size_t n) { return (unsigned)((n + kThreads - 1) / kThreads); }
 
+// The library's own stream-ordered memory pool for the current device (mpb_modexp_host), created
+// once per device with an unlimited release threshold so repeated calls reuse their allocation;
+// the device's default pool (and every other cudaMallocAsync user in the process) is untouched.
+cudaMemPool_t private_pool() {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> g(mu);
+    if (!pools[dev]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        cudaMemPool_t p = nullptr;
+        if (cudaMemPoolCreate(&p, &props) != cudaSuccess) return nullptr;
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &thr);
+        pools[dev] = p;
+    }
+    return pools[dev];
+}
+
 constexpr int kMaxLimbs = 512;  // 16384-bit operands
 // Word-sliced chunk strides are count * 16 bytes held in 32 bits (one mad.wide.u32 per address);
 // the CRT path holds 2 * count operands.
@@ -151,15 +176,14 @@ int mpb_layout_contract(const uint32_t* src, uint32_t* dst, size_t count, int li
     return check_launch();
 }
 
-// Karatsuba levels for an algo request (AUTO: the measured crossover).
-static int kara_levels(int algo, int L) {
+// Karatsuba levels for an algo request.  AUTO = schoolbook: the blocked schoolbook engine beat
+// every Karatsuba variant at every measured size on sm_100a, so no crossover exists.
+static int kara_levels(int algo, int /*L*/) {
     switch (algo) {
-        case MPB_ALGO_SCHOOLBOOK: return 0;
         case MPB_ALGO_KARATSUBA: return 1;
         case MPB_ALGO_KARATSUBA2: return 2;
-        default: return 0;  // AUTO
+        default: return 0;  // SCHOOLBOOK, AUTO
     }
-    (void)L;
 }
 
 size_t mp_batch_workspace(size_t count, int bits, int algo) {
@@ -202,8 +226,11 @@ int mp_batch_sqr(const uint32_t* a, uint32_t* c, size_t count, int bits, int alg
 }
 
 size_t mont_batch_workspace(size_t count, int bits) {
+    // T, Q word-sliced (3L per operand), or -- mont_batch_redc at the compile-time block counts --
+    // T, Q, N, N', OUT in warp tiles (6L per operand over count rounded up to 32)
     const int L = mpb_limbs(bits);
-    return count * (size_t)(3 * L) * sizeof(uint32_t);
+    const size_t sliced = count * (size_t)(3 * L), tiled = ((count + 31) & ~(size_t)31) * (size_t)(6 * L);
+    return (sliced > tiled ? sliced : tiled) * sizeof(uint32_t);
 }
 
 static bool redc_ok(int redc) { return redc == MPB_REDC_FULL || redc == MPB_REDC_TRUNCATED || redc == MPB_REDC_CIOS; }
@@ -300,8 +327,8 @@ size_t mont_batch_setup_workspace(size_t count, int bits) {
     return count * (size_t)(6 * L) * sizeof(uint32_t);
 }
 
-int mont_batch_setup(const uint32_t* N, uint32_t* NP, uint32_t* R2, size_t count, int bits, void* ws, size_t ws_bytes,
-                     void* stream) {
+static int setup_impl(const uint32_t* N, uint32_t* NP, uint32_t* R2, size_t count, int bits, int pub_bits, void* ws,
+                      size_t ws_bytes, void* stream) {
     g_err.clear();
     int L;
     if (int rc = limbs_checked(bits, L)) return rc;
@@ -312,9 +339,14 @@ int mont_batch_setup(const uint32_t* N, uint32_t* NP, uint32_t* R2, size_t count
     if (ws_bytes < mont_batch_setup_workspace(count, bits)) return fail(MPB_EINVAL, "workspace too small");
     return dispatch_L(L, [&](auto Ci, int nb) {
         constexpr int C = decltype(Ci)::value;
-        Launch<C>::setup(N, NP, R2, count, nb, (uint32_t*)ws, (cudaStream_t)stream);
+        Launch<C>::setup(N, NP, R2, count, nb, pub_bits, (uint32_t*)ws, (cudaStream_t)stream);
         return check_launch();
     });
+}
+
+int mont_batch_setup(const uint32_t* N, uint32_t* NP, uint32_t* R2, size_t count, int bits, void* ws, size_t ws_bytes,
+                     void* stream) {
+    return setup_impl(N, NP, R2, count, bits, 0, ws, ws_bytes, stream);
 }
 
 // ------------------------------------------------------------------ CRT-RSA
@@ -371,7 +403,8 @@ int rsa_batch_crt_ct(const uint32_t* c, const uint32_t* p, const uint32_t* q, co
                    cudaSuccess;
     };
     if (!concat(p, q, PQ) || !concat(dp, dq, E)) return fail(MPB_ECUDA, "device copy failed");
-    if (int rc = mont_batch_setup(PQ, NPQ, R2Q, n2, h, scr, scr_bytes, stream)) return rc;
+    // the primes' bit length is the public bits/2 (precondition), never derived from p or q
+    if (int rc = setup_impl(PQ, NPQ, R2Q, n2, h, h, scr, scr_bytes, stream)) return rc;
     int rc = dispatch_L(Lh, [&](auto Ci, int nb) {
         constexpr int C = decltype(Ci)::value;
         Launch<C>::crt_reduce(c, L, PQ, NPQ, R2Q, B, count, nb, scr, s);
@@ -401,17 +434,12 @@ int mpb_modexp_host(const uint32_t* N, const uint32_t* base, const uint32_t* exp
     const size_t ws_bytes = mont_batch_modexp_ct_workspace(count, bits, window, 0);
     const size_t setup_bytes = mont_batch_setup_workspace(count, bits);
     uint8_t* dev = nullptr;
-    {  // keep the stream-ordered pool's memory between calls (no re-mapping every call)
-        int devid = 0;
-        cudaMemPool_t pool;
-        if (cudaGetDevice(&devid) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, devid) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
-    }
+    cudaMemPool_t pool = private_pool();
+    if (!pool) return fail(MPB_ECUDA, "could not create the library's memory pool");
     // 7 arrays of L limbs (N, N', R2, base, exp, out, staging) + workspace
     const size_t total = 7 * nb + (ws_bytes > setup_bytes ? ws_bytes : setup_bytes) + 256;
-    if (cudaMallocAsync((void**)&dev, total, s) != cudaSuccess) return fail(MPB_ECUDA, "cudaMallocAsync failed");
+    if (cudaMallocFromPoolAsync((void**)&dev, total, pool, s) != cudaSuccess)
+        return fail(MPB_ECUDA, "cudaMallocFromPoolAsync failed");
     uint32_t* d[7];
     for (int i = 0; i < 7; i++) d[i] = (uint32_t*)(dev + i * nb);
     void* ws = dev + 7 * nb;

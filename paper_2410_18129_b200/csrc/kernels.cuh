@@ -149,6 +149,45 @@ __global__ void __launch_bounds__(kThreads) k_mont_redc(const uint32_t* __restri
     mont_op<C, TRUNC>(MODE_REDC, nb, T, T, arr(N, count, k), arr(NP, count, k), T, Q, arr(c, count, k), stage());
 }
 
+// warp-tiled view of operand k in an array of nch chunks per operand (DESIGN 5.6)
+MPB_DEVI ArrT tarr(uint32_t* base, int nch, size_t k) {
+    char* p = reinterpret_cast<char*>(base) + (k >> 5) * ((size_t)nch * kTileSB) + (k & 31) * 16;
+    return ArrT{p, kTileSB, 0u};
+}
+
+// Stand-alone REDC for the compile-time block counts (the hot sizes): the same engine
+// instantiation as the exponentiation's REDC / MontMul reduction phases inside k_modexp -- the
+// warp-tiled ArrT accessor, NB a compile-time constant -- so the adversarial REDC families
+// (tests/adversarial.py; Theorem 2's exact carry correction) reach the code that ships.
+// Workspace: T (2L) | Q (L) | N (L) | N' (L) | OUT (L), warp tiles over count rounded up to 32.
+template <int C, bool TRUNC, int NBT>
+__global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_mont_redc_tiled(
+    const uint32_t* __restrict__ Tin, const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP,
+    uint32_t* __restrict__ c, size_t count, uint32_t* ws) {
+    const size_t k = tid_global();
+    if (k >= count) return;
+    constexpr int Q4 = C * NBT / 4;
+    const size_t cpad = (count + 31) & ~(size_t)31;
+    uint32_t* p = ws;
+    auto take = [&](int nch) {
+        const ArrT a = tarr(p, nch, k);
+        p += cpad * (size_t)nch * 4;
+        return a;
+    };
+    const ArrT T = take(2 * Q4), Q = take(Q4), Nt = take(Q4), NPt = take(Q4), O = take(Q4);
+    const Arr Tk = arr(Tin, count, k), Nn = arr(N, count, k), NPn = arr(NP, count, k), On = arr(c, count, k);
+#pragma unroll 1
+    for (int q = 0; q < 2 * Q4; q++) T.st(q, Tk.ld(q));
+#pragma unroll 1
+    for (int q = 0; q < Q4; q++) {
+        Nt.st(q, Nn.ld(q));
+        NPt.st(q, NPn.ld(q));
+    }
+    mont_op<C, TRUNC, false, ArrT>(MODE_REDC, NBT, T, T, Nt, NPt, T, Q, O, stage());
+#pragma unroll 1
+    for (int q = 0; q < Q4; q++) On.st(q, O.ld(q));
+}
+
 // ------------------------------------------------------------------- modexp
 // alg:8FWExp as one flat, public schedule of operations so that the kernel
 // holds a single instance of the Montgomery engine:
@@ -175,11 +214,6 @@ __global__ void __launch_bounds__(kThreads) k_mont_redc(const uint32_t* __restri
 // slower with it (1536 / 2560 / 4108 bits: 5-20 %) and keep the word-sliced workspace
 __host__ __device__ constexpr bool modexp_tiled(int KLEV, bool TMA, int NBT) {
     return MPB_TILE && KLEV == 0 && !TMA && NBT != 0;
-}
-// warp-tiled view of operand k in an array of nch chunks per operand
-MPB_DEVI ArrT tarr(uint32_t* base, int nch, size_t k) {
-    char* p = reinterpret_cast<char*>(base) + (k >> 5) * ((size_t)nch * kTileSB) + (k & 31) * 16;
-    return ArrT{p, kTileSB, 0u};
 }
 template <int C, int RM, int NBT, int KLEV, bool COOP, bool TMA = false>
 MPB_DEVI void modexp_body(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
@@ -364,13 +398,17 @@ __global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_modexp_coop(
 // N' = (-N)^-1 mod R and R^2 mod N (mp_setup.cuh); workspace 6L words per operand.
 template <int C>
 __global__ void __launch_bounds__(kThreads) k_setup(const uint32_t* __restrict__ N, uint32_t* __restrict__ NP,
-                                                    uint32_t* __restrict__ R2, size_t count, int nb, uint32_t* ws) {
+                                                    uint32_t* __restrict__ R2, size_t count, int nb, int pub_bits,
+                                                    uint32_t* ws) {
     const size_t k = tid_global();
     if (k >= count) return;
     const int L = C * nb;
-    int top = L - 1;  // bit length of the (public) modulus
-    while (top > 0 && word_at(N, count, k, top) == 0) top--;
-    const int nbits = 32 * top + (32 - __clz(word_at(N, count, k, top)));
+    int nbits = pub_bits;  // the public bit length (CRT primes: bits/2, never read from the secret)
+    if (nbits <= 0) {      // a public modulus: its bit length from its top limbs
+        int top = L - 1;
+        while (top > 0 && word_at(N, count, k, top) == 0) top--;
+        nbits = 32 * top + (32 - __clz(word_at(N, count, k, top)));
+    }
     setup_one<C>(nb, arr(N, count, k), arr(NP, count, k), arr(R2, count, k), arr(ws, count, k), stage(),
                  word_at(N, count, k, 0), nbits);
 }
@@ -509,10 +547,10 @@ __global__ void __launch_bounds__(kThreads) k_crt_recombine(const uint32_t* __re
 
 // ---------------------------------------------------------------- launchers
 template <int C>
-void Launch<C>::setup(const uint32_t* N, uint32_t* NP, uint32_t* R2, size_t count, int nb, uint32_t* ws,
-                      cudaStream_t s) {
+void Launch<C>::setup(const uint32_t* N, uint32_t* NP, uint32_t* R2, size_t count, int nb, int pub_bits,
+                      uint32_t* ws, cudaStream_t s) {
     k_setup<C><<<(unsigned)((count + kThreads - 1) / kThreads), kThreads, stage_bytes<C>(), s>>>(N, NP, R2, count, nb,
-                                                                                               ws);
+                                                                                               pub_bits, ws);
 }
 
 inline unsigned grid_for(size_t n) { return (unsigned)((n + kThreads - 1) / kThreads); }
@@ -588,8 +626,16 @@ template <int C>
 void Launch<C>::mont_redc(const uint32_t* T, const uint32_t* N, const uint32_t* NP, uint32_t* c, size_t count, int nb,
                           bool trunc, uint32_t* ws, cudaStream_t s) {
     const size_t sm = stage_bytes<C>();
-    if (trunc) k_mont_redc<C, true><<<grid_for(count), kThreads, sm, s>>>(T, N, NP, c, count, nb, ws);
-    else k_mont_redc<C, false><<<grid_for(count), kThreads, sm, s>>>(T, N, NP, c, count, nb, ws);
+    with_nb<C>(nb, [&](auto NBc) {
+        constexpr int NBT = decltype(NBc)::value;
+        if constexpr (NBT != 0 && MPB_TILE) {  // the exponentiation's tiled, compile-time-NB engine
+            if (trunc) k_mont_redc_tiled<C, true, NBT><<<grid_for(count), kThreads, sm, s>>>(T, N, NP, c, count, ws);
+            else k_mont_redc_tiled<C, false, NBT><<<grid_for(count), kThreads, sm, s>>>(T, N, NP, c, count, ws);
+        } else {
+            if (trunc) k_mont_redc<C, true><<<grid_for(count), kThreads, sm, s>>>(T, N, NP, c, count, nb, ws);
+            else k_mont_redc<C, false><<<grid_for(count), kThreads, sm, s>>>(T, N, NP, c, count, nb, ws);
+        }
+    });
 }
 // One-thread or cooperative kernel (small >= 3072-bit batches); MPB_COOP=0 / 1 forces never /
 // always (tuning and tests).

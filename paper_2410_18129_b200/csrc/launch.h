@@ -25,9 +25,11 @@ struct Launch {
     static void crt_recombine(const uint32_t* M, const uint32_t* PQ, const uint32_t* NPQ, const uint32_t* R2Q,
                               const uint32_t* qinv, uint32_t* out, int Lo, size_t count, int nb, uint32_t* ws,
                               cudaStream_t s);
-    // N' = (-N)^-1 mod R and R^2 mod N; ws: 6L words per operand
-    static void setup(const uint32_t* N, uint32_t* NP, uint32_t* R2, size_t count, int nb, uint32_t* ws,
-                      cudaStream_t s);
+    // N' = (-N)^-1 mod R and R^2 mod N; ws: 6L words per operand.  pub_bits > 0: every modulus has
+    // exactly this (public) bit length (CRT primes: the schedule must not depend on a secret
+    // length); 0: each modulus's bit length is read from its top limbs (public moduli)
+    static void setup(const uint32_t* N, uint32_t* NP, uint32_t* R2, size_t count, int nb, int pub_bits,
+                      uint32_t* ws, cudaStream_t s);
     // levels: Karatsuba levels of the product phases (0 = schoolbook)
     static void modexp(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
                        const uint32_t* exp, uint32_t* out, size_t count, int nb, int bits, int window, int redc,

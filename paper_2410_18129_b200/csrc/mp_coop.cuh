@@ -178,9 +178,12 @@ MPB_DEVI void engine_coop(int ph, int NB, const AR& AX, const AR& AY, const AR& 
             }
         }
         if (nk != k) {  // ---- end of block column k: both lanes hold the column total
+            // Invariant: only role 0 stores (DST, T, OUT) and only role 0 reads T blocks that this
+            // phase rewrites; role 1's column results are discarded (its window is cleared below)
+            // and the phase ends with __syncwarp, so no lane reads a block the other is storing.
             coop_window_sum<C>(W, mask);
             if (ph != PH_HI) {
-                stb<C>(DST, k, W);
+                if (role == 0) stb<C>(DST, k, W);
                 w_shift<C>(W);
             } else if (TRUNC) {
                 if (k == NB - 1) {
@@ -198,7 +201,12 @@ MPB_DEVI void engine_coop(int ph, int NB, const AR& AX, const AR& AY, const AR& 
                 }
             } else {
                 uint32_t tb[C];
-                ldb<C>(T, k, tb);
+                if (role == 0) {
+                    ldb<C>(T, k, tb);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < C; i++) tb[i] = 0;
+                }
                 add_first(W[0], tb[0]);
 #pragma unroll
                 for (int i = 1; i < C; i++) add_next(W[i], tb[i]);
@@ -216,7 +224,7 @@ MPB_DEVI void engine_coop(int ph, int NB, const AR& AX, const AR& AY, const AR& 
     }
     // the top of the walk: role 1's window is zero, role 0 holds it; make both hold it
     coop_window_sum<C>(W, mask);
-    if (ph == PH_MUL || ph == PH_SQR) stb<C>(DST, 2 * NB - 1, W);
+    if ((ph == PH_MUL || ph == PH_SQR) && role == 0) stb<C>(DST, 2 * NB - 1, W);
     if (ph == PH_Q) {  // both roles need c_add / the correction inputs
         orlo |= __shfl_xor_sync(mask, orlo, 1);
         tl1 |= __shfl_xor_sync(mask, tl1, 1);
@@ -226,7 +234,12 @@ MPB_DEVI void engine_coop(int ph, int NB, const AR& AX, const AR& AY, const AR& 
             emit_block<C>(W, NB - 1, NB, true, T, N, OUT, carry, borrow, role == 0);
         } else {
             uint32_t tb[C];
-            ldb<C>(T, 2 * NB - 1, tb);
+            if (role == 0) {
+                ldb<C>(T, 2 * NB - 1, tb);
+            } else {
+#pragma unroll
+                for (int i = 0; i < C; i++) tb[i] = 0;
+            }
             add_first(W[0], tb[0]);
 #pragma unroll
             for (int i = 1; i < C; i++) add_next(W[i], tb[i]);

@@ -30,6 +30,13 @@
 
 namespace mpb {
 
+#ifdef MPB_CORR_COUNT
+// DEBUG builds only (csrc/debug/corr_count.cu -> libmpb_corr.so, a test artefact): how many times
+// the exact carry correction of Theorem 2 ([S mod 2^32 > K]) evaluated to 1.  The
+// counting branch depends on secret data, so no shipped build defines MPB_CORR_COUNT.
+static __device__ unsigned long long g_corr_count;
+#endif
+
 // ----------------------------------------------------------------- accessors
 // Word-sliced global array: chunk q (4 limbs, 16 bytes) of this thread's number at p + q*sb
 // (sb = count * 16 bytes).  The chunk address is one IMAD.WIDE.U32 (32-bit q times 32-bit sb
@@ -161,6 +168,9 @@ MPB_DEVI void w_shift(uint32_t (&W)[2 * C + 1]) {  // W >>= 32C
 // ------------------------------------------------ shared tail: C, D = C - N
 // Block j of H (window words 0..C-1) becomes block j of C = T_hi + H + carry (truncated) or
 // of C itself (full); C is parked in T block NB+j and D = C - N - borrow goes to OUT block j.
+// wr = false (the idle lane of a cooperative pair, mp_coop.cuh): nothing is stored and T is not
+// read (zeros instead) -- that lane's results are discarded, and reading T here would race with
+// the partner lane's store of the same block.
 template <int C, class AR = Arr>
 MPB_DEVI void emit_block(const uint32_t (&W)[2 * C + 1], int j, int NB, bool add_thi, const AR& T, const AR& N,
                          const AR& OUT, uint32_t& carry, uint32_t& borrow, bool wr = true) {
@@ -169,7 +179,12 @@ MPB_DEVI void emit_block(const uint32_t (&W)[2 * C + 1], int j, int NB, bool add
     for (int i = 0; i < C; i++) c[i] = W[i];
     if (add_thi) {
         uint32_t t[C];
-        ldb<C>(T, NB + j, t);
+        if (wr) {
+            ldb<C>(T, NB + j, t);
+        } else {
+#pragma unroll
+            for (int i = 0; i < C; i++) t[i] = 0;
+        }
         cc_restore(carry);
 #pragma unroll
         for (int i = 0; i < C; i++) add_next(c[i], t[i]);
@@ -408,6 +423,9 @@ MPB_DEVI void engine(int ph, int NB, const AR& AX, const AR& AY, const AR& DST, 
                 if (k == NB - 1) {
                     // exact carry out of column L-1: floor(S/2^32) + [S mod 2^32 > K]
                     const uint32_t corr = W[0] > orlo ? 1u : 0u;
+#ifdef MPB_CORR_COUNT
+                    if (corr) atomicAdd(&g_corr_count, 1ull);
+#endif
 #pragma unroll
                     for (int i = 0; i < 2 * C; i++) W[i] = W[i + 1];
                     W[2 * C] = 0;

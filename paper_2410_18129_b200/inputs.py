@@ -118,6 +118,28 @@ def modexp_inputs(config: int, count: int, bits: int, dataset: int = 0):
     return N, base, exp
 
 
+CHUNK = 1 << 16  # operands per independently seeded chunk of a sliced global batch (config 5)
+
+
+def modexp_inputs_range(config: int, start: int, stop: int, bits: int, chunk: int = CHUNK):
+    """Operands [start, stop) of a global modexp batch drawn chunk by chunk: chunk c (operands
+    c*chunk .. (c+1)*chunk-1) is modexp_inputs(config, chunk, bits, dataset=c).  A rank generates
+    only the chunks its slice touches, and every slicing of the global batch sees the same operands
+    (config 5: "generated once and sliced", G-invariance)."""
+    if not 0 <= start <= stop:
+        raise ValueError("need 0 <= start <= stop")
+    L = limbs_for_bits(bits)
+    parts = ([], [], [])
+    for c in range(start // chunk, (stop + chunk - 1) // chunk):
+        lo, hi = max(start, c * chunk) - c * chunk, min(stop, (c + 1) * chunk) - c * chunk
+        for p, x in zip(parts, modexp_inputs(config, chunk, bits, dataset=c)):
+            p.append(x[lo:hi])
+    if not parts[0]:
+        z = np.zeros((0, L), np.uint32)
+        return z, z.copy(), z.copy()
+    return tuple(np.concatenate(p) for p in parts)
+
+
 def montmul_inputs(config: int, count: int, bits: int, dataset: int = 0):
     """(N, a, b) for a Montgomery multiply/square batch: shapes (count, L)."""
     rng = rng_for(config, dataset)

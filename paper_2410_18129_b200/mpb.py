@@ -102,6 +102,24 @@ def _sliced_shape(t: torch.Tensor) -> tuple[int, int]:
     return 4 * t.shape[0], t.shape[1]
 
 
+def _expect(t: torch.Tensor | None, L: int, count: int, name: str) -> None:
+    """t must be word-sliced with exactly L limbs and `count` operands (the kernels index every
+    array with the same L and count: a mismatch would read or write outside the allocation)."""
+    if t is None:
+        raise ValueError(f"{name} is required")
+    shape = tuple(t.shape)
+    if shape != (L // 4, count, 4):
+        raise ValueError(f"{name}: expected word-sliced shape {(L // 4, count, 4)}, got {shape}")
+
+
+def _limbs_for(bits: int, L: int, what: str = "operands") -> None:
+    Lb = _lib.mpb_limbs(bits)
+    if Lb <= 0:
+        raise ValueError(f"bits must be positive (got {bits})")
+    if Lb != L:
+        raise ValueError(f"bits={bits} needs {Lb}-limb {what}, got {L} limbs")
+
+
 def empty_sliced(L: int, count: int, device="cuda") -> torch.Tensor:
     return torch.empty((L // 4, count, 4), dtype=torch.int32, device=device)
 
@@ -136,6 +154,8 @@ def mp_workspace(count: int, bits: int, algo: int, device="cuda") -> torch.Tenso
 def mp_batch_mul(a: torch.Tensor, b: torch.Tensor, bits: int, algo: int = ALGO_AUTO,
                  ws: torch.Tensor | None = None) -> torch.Tensor:
     L, count = _sliced_shape(a)
+    _limbs_for(bits, L)
+    _expect(b, L, count, "b")
     ws = ws if ws is not None else mp_workspace(count, bits, algo, a.device)
     c = empty_sliced(2 * L, count, a.device)
     _check(_lib.mp_batch_mul(_ptr(a), _ptr(b), _ptr(c), count, bits, algo, _ptr(ws),
@@ -145,6 +165,7 @@ def mp_batch_mul(a: torch.Tensor, b: torch.Tensor, bits: int, algo: int = ALGO_A
 
 def mp_batch_sqr(a: torch.Tensor, bits: int, algo: int = ALGO_AUTO, ws: torch.Tensor | None = None) -> torch.Tensor:
     L, count = _sliced_shape(a)
+    _limbs_for(bits, L)
     ws = ws if ws is not None else mp_workspace(count, bits, algo, a.device)
     c = empty_sliced(2 * L, count, a.device)
     _check(_lib.mp_batch_sqr(_ptr(a), _ptr(c), count, bits, algo, _ptr(ws), 0 if ws is None else ws.numel() * 4,
@@ -158,6 +179,9 @@ def mont_workspace(count: int, bits: int, device="cuda") -> torch.Tensor:
 
 def mont_batch_mul(a, b, N, Np, bits: int, redc: int = REDC_TRUNCATED, ws: torch.Tensor | None = None):
     L, count = _sliced_shape(a)
+    _limbs_for(bits, L)
+    for t, name in ((b, "b"), (N, "N"), (Np, "Np")):
+        _expect(t, L, count, name)
     ws = ws if ws is not None else mont_workspace(count, bits, a.device)
     c = empty_sliced(L, count, a.device)
     _check(_lib.mont_batch_mul(_ptr(a), _ptr(b), _ptr(N), _ptr(Np), _ptr(c), count, bits, redc, _ptr(ws),
@@ -167,6 +191,9 @@ def mont_batch_mul(a, b, N, Np, bits: int, redc: int = REDC_TRUNCATED, ws: torch
 
 def mont_batch_sqr(a, N, Np, bits: int, redc: int = REDC_TRUNCATED, ws: torch.Tensor | None = None):
     L, count = _sliced_shape(a)
+    _limbs_for(bits, L)
+    for t, name in ((N, "N"), (Np, "Np")):
+        _expect(t, L, count, name)
     ws = ws if ws is not None else mont_workspace(count, bits, a.device)
     c = empty_sliced(L, count, a.device)
     _check(_lib.mont_batch_sqr(_ptr(a), _ptr(N), _ptr(Np), _ptr(c), count, bits, redc, _ptr(ws), ws.numel() * 4,
@@ -176,6 +203,9 @@ def mont_batch_sqr(a, N, Np, bits: int, redc: int = REDC_TRUNCATED, ws: torch.Te
 
 def mont_batch_redc(T, N, Np, bits: int, redc: int = REDC_TRUNCATED, ws: torch.Tensor | None = None):
     L, count = _sliced_shape(N)
+    _limbs_for(bits, L)
+    _expect(Np, L, count, "Np")
+    _expect(T, 2 * L, count, "T")
     ws = ws if ws is not None else mont_workspace(count, bits, N.device)
     c = empty_sliced(L, count, N.device)
     _check(_lib.mont_batch_redc(_ptr(T), _ptr(N), _ptr(Np), _ptr(c), count, bits, redc, _ptr(ws), ws.numel() * 4,
@@ -185,6 +215,7 @@ def mont_batch_redc(T, N, Np, bits: int, redc: int = REDC_TRUNCATED, ws: torch.T
 
 def mont_batch_setup(N: torch.Tensor, bits: int) -> tuple[torch.Tensor, torch.Tensor]:
     L, count = _sliced_shape(N)
+    _limbs_for(bits, L)
     Np, R2 = empty_sliced(L, count, N.device), empty_sliced(L, count, N.device)
     ws = workspace(_lib.mont_batch_setup_workspace(count, bits), N.device)
     _check(_lib.mont_batch_setup(_ptr(N), _ptr(Np), _ptr(R2), count, bits, _ptr(ws), ws.numel() * 4, _stream()))
@@ -198,7 +229,12 @@ def modexp_workspace(count: int, bits: int, window: int, algo: int = ALGO_AUTO, 
 def mont_batch_modexp_ct(N, Np, R2, base, exp, bits: int, window: int = 5, redc: int = REDC_TRUNCATED,
                          algo: int = ALGO_AUTO, ws: torch.Tensor | None = None, out: torch.Tensor | None = None):
     L, count = _sliced_shape(N)
+    _limbs_for(bits, L)
+    for t, name in ((Np, "Np"), (R2, "R2"), (base, "base"), (exp, "exp")):
+        _expect(t, L, count, name)
     ws = ws if ws is not None else modexp_workspace(count, bits, window, algo, N.device)
+    if out is not None:
+        _expect(out, L, count, "out")
     out = out if out is not None else empty_sliced(L, count, N.device)
     _check(_lib.mont_batch_modexp_ct(_ptr(N), _ptr(Np), _ptr(R2), _ptr(base), _ptr(exp), _ptr(out), count, bits,
                                      window, redc, algo, _ptr(ws), ws.numel() * 4, _stream()))
@@ -213,7 +249,13 @@ def rsa_batch_crt_ct(c, p, q, dp, dq, qinv, bits: int, window: int = 5, redc: in
                      ws: torch.Tensor | None = None, out: torch.Tensor | None = None):
     """m = c^d mod pq by CRT (word-sliced: c with L(bits) limbs, p/q/dp/dq/qinv with L(bits/2))."""
     L, count = _sliced_shape(c)
+    _limbs_for(bits, L)
+    Lh = _lib.mpb_limbs(bits // 2)
+    for t, name in ((p, "p"), (q, "q"), (dp, "dp"), (dq, "dq"), (qinv, "qinv")):
+        _expect(t, Lh, count, name)
     ws = ws if ws is not None else rsa_workspace(count, bits, window, c.device)
+    if out is not None:
+        _expect(out, L, count, "out")
     out = out if out is not None else empty_sliced(L, count, c.device)
     _check(_lib.rsa_batch_crt_ct(_ptr(c), _ptr(p), _ptr(q), _ptr(dp), _ptr(dq), _ptr(qinv), _ptr(out), count, bits,
                                  window, redc, _ptr(ws), ws.numel() * 4, _stream()))
@@ -224,11 +266,23 @@ def modexp_host(N: np.ndarray, base: np.ndarray, exp: np.ndarray, bits: int, win
                 redc: int = REDC_TRUNCATED) -> np.ndarray:
     """End-to-end over host buffers (operand-major uint32 (count, L)); blocking."""
     N, base, exp = (np.ascontiguousarray(x, dtype=np.uint32) for x in (N, base, exp))
+    if N.ndim != 2:
+        raise ValueError("operand-major arrays have shape (count, L)")
     count, L = N.shape
+    _limbs_for(bits, L)
+    if base.shape != N.shape or exp.shape != N.shape:
+        raise ValueError(f"N, base and exp must all have shape {N.shape}, got {base.shape} and {exp.shape}")
     out = np.empty_like(N)
     _check(_lib.mpb_modexp_host(N.ctypes.data, base.ctypes.data, exp.ctypes.data, out.ctypes.data, count, bits,
                                 window, redc, _stream()))
     return out
+
+
+def modexp_host_ptrs(N: int, base: int, exp: int, out: int, count: int, bits: int, window: int, redc: int,
+                     stream: int) -> None:
+    """mpb_modexp_host on raw host pointers (operand-major, count x mpb_limbs(bits) limbs each; the
+    caller guarantees the sizes) and an explicit cudaStream_t handle (multi-device drivers)."""
+    _check(_lib.mpb_modexp_host(N, base, exp, out, count, bits, window, redc, stream))
 
 
 # ------------------------------------------------------- host <-> device

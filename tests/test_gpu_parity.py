@@ -15,7 +15,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from adversarial import redc_family
+from adversarial import redc_family, t_gamma
 from paper_2410_18129_b200 import inputs as I
 
 pytestmark = pytest.mark.gpu
@@ -148,6 +148,104 @@ def test_mont_redc_adversarial(mpb, bits, redc):
     c = mpb.to_host(mpb.mont_batch_redc(mpb.to_device(T), dN, Np, bits, redc=redc))
     for k in range(count):
         assert I.from_limbs(c[k]) == O.redc(Ts[k], Ns[k], L), k
+
+
+def _gamma_low(rng: random.Random, N: int, L: int, k: int) -> int:
+    """A gamma-family T (forced wrap of column L-1, tests/adversarial.py) with a zero high half
+    and T < N, so it is a valid operand in the R^2 position of the exponentiation."""
+    R = 1 << (32 * L)
+    while True:
+        t = t_gamma(rng, N, L, k) % R
+        if t < N:
+            return t
+
+
+def _schedule_modexp(base: int, e: int, N: int, rho: int, L: int, bits: int, w: int) -> int:
+    """alg:8FWExp's public schedule as k_modexp runs it (kernels.cuh; reading A11: G[0] =
+    REDC(R2), G[1] = MontMul(base, R2), G[i] = MontMul(G[i-1], G[1]), LSB-aligned windows, the top
+    window selects the start, w squarings + one multiplication per window, REDC at the end), every
+    Montgomery operation at its definition x*y*R^-1 mod N, with `rho` in the R^2 position."""
+    R = 1 << (32 * L)
+    Ri = pow(R, -1, N)
+
+    def mm(x, y):
+        return x * y * Ri % N
+
+    G = [rho * Ri % N, mm(base, rho)]
+    for _ in range(2, 1 << w):
+        G.append(mm(G[-1], G[1]))
+    nwin = -(-bits // w)
+    dig = [(e >> (i * w)) & ((1 << w) - 1) for i in range(nwin)]
+    Y = G[dig[-1]]
+    for j in range(nwin - 2, -1, -1):
+        for _ in range(w):
+            Y = mm(Y, Y)
+        Y = mm(Y, G[dig[j]])
+    return Y * Ri % N
+
+
+def _corr_lib():
+    import ctypes
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.abspath(I.__file__)), "libmpb_corr.so")
+    if not os.path.exists(path):
+        raise AssertionError(f"{path} missing: build() builds it beside libmpb.so")
+    lib = ctypes.CDLL(path)
+    lib.mpb_corr_modexp_2048.restype = ctypes.c_int
+    lib.mpb_corr_modexp_2048.argtypes = [ctypes.c_void_p] * 6 + [ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p,
+                                                                  ctypes.c_void_p]
+    lib.mpb_corr_count_take.restype = ctypes.c_ulonglong
+    return lib
+
+
+def test_theorem2_correction_fires_in_shipped_modexp_kernel(mpb):
+    """Theorem 2's exact carry correction exercised deterministically in
+    the instantiation bench.py times, k_modexp<C=16, truncated, NB=4, schoolbook> on the warp-tiled
+    workspace: a gamma-family T (S mod 2^32 = 2^32-1-k, T < N) in the R^2 position makes the
+    exponentiation's first operation, REDC(R2), need the correction.  (1) The release library's
+    output equals the exact schedule for every operand (and the schedule model itself reduces to
+    base^e mod N when R2 = R^2 mod N).  (2) The same kernel built with the correction counter
+    (libmpb_corr.so) reports that the correction fired at least once per crafted operand."""
+    import ctypes
+
+    bits, w, count = 2048, 5, 40  # ragged: one full warp tile and a partial one
+    L = I.limbs_for_bits(bits)
+    R = 1 << (32 * L)
+    N, base, exp = I.modexp_inputs(config=3, count=count, bits=bits, dataset=7)
+    Ns, Bs, Es = ints(N), ints(base), ints(exp)
+    rng = random.Random(2410)
+    crafted = list(range(0, count, 2))  # even operands crafted, odd ones keep R^2 mod N
+    rho = [(_gamma_low(rng, n, L, k % 3) if k in crafted else R * R % n) for k, n in enumerate(Ns)]
+    assert _schedule_modexp(Bs[1], Es[1], Ns[1], rho[1], L, bits, w) == pow(Bs[1], Es[1], Ns[1])
+    dN, dB, dE = (mpb.to_device(x) for x in (N, base, exp))
+    Np, _ = mpb.mont_batch_setup(dN, bits)
+    dR = mpb.to_device(I.ints_to_array(rho, L))
+    out = mpb.to_host(mpb.mont_batch_modexp_ct(dN, Np, dR, dB, dE, bits, w, redc=mpb.REDC_TRUNCATED))
+    for k in range(count):
+        assert I.from_limbs(out[k]) == _schedule_modexp(Bs[k], Es[k], Ns[k], rho[k], L, bits, w), k
+    # full REDC on the same inputs agrees (it has no correction term)
+    out_f = mpb.to_host(mpb.mont_batch_modexp_ct(dN, Np, dR, dB, dE, bits, w, redc=mpb.REDC_FULL))
+    assert np.array_equal(out, out_f)
+    # the counter build of the same kernel
+    lib = _corr_lib()
+    torch.cuda.synchronize()
+    lib.mpb_corr_count_take()
+    ws = mpb.modexp_workspace(count, bits, w)
+    o2 = mpb.empty_sliced(L, count)
+    rc = lib.mpb_corr_modexp_2048(dN.data_ptr(), Np.data_ptr(), dR.data_ptr(), dB.data_ptr(), dE.data_ptr(),
+                                  o2.data_ptr(), count, w, ws.data_ptr(), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0
+    fired = lib.mpb_corr_count_take()
+    assert np.array_equal(mpb.to_host(o2), out)
+    assert fired >= len(crafted), fired
+    # control: no crafted operand -> (almost surely) no correction in this small batch
+    dR0 = mpb.to_device(I.ints_to_array([R * R % n for n in Ns], L))
+    rc = lib.mpb_corr_modexp_2048(dN.data_ptr(), Np.data_ptr(), dR0.data_ptr(), dB.data_ptr(), dE.data_ptr(),
+                                  o2.data_ptr(), count, w, ws.data_ptr(), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0
+    assert lib.mpb_corr_count_take() < len(crafted)
+    assert np.array_equal(mpb.to_host(o2), O.batch_modexp(base, exp, bits, N))
 
 
 # ------------------------------------------------------------------- modexp
