@@ -1,0 +1,156 @@
+// inst_D52.cu -- the radix-2^52 FP64 exponentiation (mp_dfma.cuh), selected by
+// mont_batch_modexp_ct with algo = MPB_ALGO_RADIX52.  Same ABI, same inputs (32-bit word-sliced
+// N, N', R^2 mod N, base, exp) and the same canonical result as the 32-bit kernels; only the
+// internal radix differs.
+#include "kernels.cuh"
+#include "mp_dfma.cuh"
+
+namespace mpb {
+
+// Internal constants from the ABI's 32-bit ones (R32 = 2^(32L), R52 = 2^(52D)):
+//   N'52 = -N^-1 mod R52 by one Newton step from N'32: x0 = -N'32 (= N^-1 mod R32),
+//          x1 = x0 (2 - N x0) mod R52 (exact to 2^(64L) >= R52), N'52 = -x1
+//   R52^2 mod N = MontSqr52(MontMul52(R2_32, 2^k)), k = 130 D - 64 L  (0 <= k <= bits - 2):
+//          MontMul52(a, b) = a b 2^(-52D), so 2^(64L + k - 52D) squared is 2^(128L + 2k - 156D) = 2^(104D)
+// Then alg:8FWExp exactly as k_modexp: G[0] = REDC(R^2), G[1] = MontMul(base, R^2),
+// G[e] = MontMul(G[e-1], G[1]), top window by CT select, w squarings + select + multiply per window,
+// REDC, and one masked subtraction to [0, N) at the end (operands live in [0, 2N), R52 >= 4N).
+// Workspace (warp tiles over count rounded up to 32, D/2 chunks of 16 bytes per number):
+//   G (2^w numbers) | Y | T (2 numbers) | Q | S | N | N' | X
+template <int C, int NB, bool TRUNC>
+__global__ void __launch_bounds__(kThreads, 3) k_modexp_d52(const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP,
+                                                          const uint32_t* __restrict__ R2, const uint32_t* __restrict__ base,
+                                                          const uint32_t* __restrict__ exp, uint32_t* __restrict__ out,
+                                                          size_t count, int L, int bits, int w, uint32_t* ws) {
+    namespace d = d52;
+    const size_t k = tid_global();
+    if (k >= count) return;
+    constexpr int D = C * NB, QD = D / 2;
+    const int nent = 1 << w;
+    const size_t cpad = (count + 31) & ~(size_t)31;
+    uint32_t* p = ws;
+    auto take = [&](int nch) {
+        const ArrT a = tarr(p, nch, k);
+        p += cpad * (size_t)nch * 4;
+        return a;
+    };
+    const ArrT G = take(nent * QD), Y = take(QD), T = take(2 * QD), Q = take(QD), S = take(QD), Nt = take(QD),
+               NPt = take(QD), X = take(QD);
+    const Stage sg = stage();
+    auto zext_to_T = [&](const ArrT& a) {  // T = a zero-extended to 2D limbs (REDC input)
+#pragma unroll 1
+        for (int q = 0; q < QD; q++) {
+            T.st(q, a.ld(q));
+            T.st(QD + q, make_uint4(0, 0, 0, 0));
+        }
+    };
+    const int nwin = (bits + w - 1) / w;
+    auto window = [&](int win) {
+        const int pos = win * w, wi = pos >> 5, off = pos & 31;
+        uint32_t v = word_at(exp, count, k, wi) >> off;
+        if (off + w > 32 && wi + 1 < L) v |= word_at(exp, count, k, wi + 1) << (32 - off);
+        return v & ((1u << w) - 1u);
+    };
+    // One flat public schedule with a single Montgomery call site (as k_modexp):
+    //   0  S = N x0 mod R52 (LO)          1  Y = x0 (2 - S) mod R52 (LO)
+    //   2  Y = MontMul(R2_32, 2^k)         3  S = MontSqr(Y) = R52^2 mod N
+    //   4  G[0] = REDC(S)                  5  G[1] = MontMul(base, S)
+    //   4 + e (e = 2 .. 2^w - 1)  G[e] = MontMul(G[e-1], G[1])
+    //   then per window: w x MontSqr(Y), select, MontMul(Y, S); the top window selects the start
+    //   last  S = REDC(Y), canonical, back to 32-bit limbs
+    const int n_pre = 4 + nent;
+    const int per_win = w + 1;
+    const int n_ops = n_pre + (nwin - 1) * per_win + 1;
+#pragma unroll 1
+    for (int op = 0; op < n_ops; op++) {
+        int mode = d::MODE_MUL;
+        ArrT A = Y, B = S, O = Y;
+        if (op < n_pre) {
+            if (op == 0) {
+                d::from32<D>(arr(N, count, k), L, Nt);
+                d::from32<D>(arr(NP, count, k), L, X);
+                d::sub_from<D>(0, X, X);  // x0 = -N'32 mod R52 (= N^-1 mod R32)
+                mode = d::MODE_LO; A = Nt; B = X; O = S;
+            } else if (op == 1) {
+                d::sub_from<D>(2, S, S);
+                mode = d::MODE_LO; A = X; B = S; O = Y;  // x1 = N^-1 mod R52
+            } else if (op == 2) {
+                d::sub_from<D>(0, Y, NPt);  // N'52 = -x1
+                d::from32<D>(arr(R2, count, k), L, X);
+                d::set_pow2<D>(130 * D - 64 * L, S);
+                A = X; B = S; O = Y;
+            } else if (op == 3) {
+                mode = d::MODE_SQR; A = Y; B = Y; O = S;
+            } else if (op == 4) {
+                zext_to_T(S);
+                mode = d::MODE_REDC; A = T; B = T; O = G;
+            } else if (op == 5) {
+                d::from32<D>(arr(base, count, k), L, X);
+                A = X; B = S; O = G.at(QD);
+            } else {
+                const int e = op - 4;
+                A = G.at((e - 1) * QD); B = G.at(QD); O = G.at(e * QD);
+            }
+            if (op == n_pre - 1) {  // after the table: the top window selects the start value
+                d::mont_op<C, NB, TRUNC>(mode, A, B, Nt, NPt, T, Q, O, sg);
+                ct_select<4, 4>(G, 2 * D, nent, window(nwin - 1), Y);
+                continue;
+            }
+        } else if (op == n_ops - 1) {
+            zext_to_T(Y);
+            mode = d::MODE_REDC; A = T; B = T; O = S;
+        } else {
+            const int r = (op - n_pre) % per_win, win = nwin - 2 - (op - n_pre) / per_win;
+            if (r < w) {
+                mode = d::MODE_SQR; A = Y; B = Y; O = Y;
+            } else {
+                ct_select<4, 4>(G, 2 * D, nent, window(win), S);
+                A = Y; B = S; O = Y;
+            }
+        }
+        d::mont_op<C, NB, TRUNC>(mode, A, B, Nt, NPt, T, Q, O, sg);
+    }
+    // ---- canonical [0, N), back to 32-bit limbs
+    d::final_sub<D>(S, Nt, Q, X);
+    d::to32<D>(X, L, arr(out, count, k));
+}
+
+// (C, NB) instances: 1024 (4, 5) D = 20; 2048 (8, 5) D = 40; 3072 (8, 8) D = 64; 4096 / 4108 (8, 10) D = 80
+int d52_digits(int bits) {
+    const int L = 4 * ((bits + 127) / 128);
+    for (int D : {20, 40, 64, 80}) {
+        const int kk = 130 * D - 64 * L;
+        if (52 * D >= bits + 2 && kk >= 0 && kk <= bits - 2) return D;
+    }
+    return 0;
+}
+
+size_t d52_workspace_bytes(size_t count, int bits, int window) {
+    const int D = d52_digits(bits);
+    if (!D) return 0;
+    const size_t cpad = (count + 31) & ~(size_t)31;
+    return cpad * (size_t)(D / 2) * 16 * (size_t)((1 << window) + 8);
+}
+
+bool launch_modexp_d52(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
+                       const uint32_t* exp, uint32_t* out, size_t count, int bits, int window, bool trunc,
+                       uint32_t* ws, cudaStream_t s) {
+    const int L = 4 * ((bits + 127) / 128);
+    const unsigned g = (unsigned)((count + kThreads - 1) / kThreads);
+    const size_t sm = (size_t)kThreads * 4 * 4 * 16;  // 2 buffers x 2 blocks x (C/2 <= 4) chunks
+    auto go = [&](auto Cc, auto NBc) {
+        constexpr int C = decltype(Cc)::value, NBv = decltype(NBc)::value;
+        if (trunc) k_modexp_d52<C, NBv, true><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, L, bits, window, ws);
+        else k_modexp_d52<C, NBv, false><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, L, bits, window, ws);
+        return true;
+    };
+    switch (d52_digits(bits)) {
+        case 20: return go(std::integral_constant<int, 4>{}, std::integral_constant<int, 5>{});
+        case 40: return go(std::integral_constant<int, 8>{}, std::integral_constant<int, 5>{});
+        case 64: return go(std::integral_constant<int, 8>{}, std::integral_constant<int, 8>{});
+        case 80: return go(std::integral_constant<int, 8>{}, std::integral_constant<int, 10>{});
+        default: return false;
+    }
+}
+
+}  // namespace mpb

@@ -215,11 +215,12 @@ __global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_mont_redc_tiled(
 __host__ __device__ constexpr bool modexp_tiled(int KLEV, bool TMA, int NBT) {
     return MPB_TILE && KLEV == 0 && !TMA && NBT != 0;
 }
-template <int C, int RM, int NBT, int KLEV, bool COOP, bool TMA = false>
+template <int C, int RM, int NBT, int KLEV, int LANES, bool TMA = false>
 MPB_DEVI void modexp_body(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
                           const uint32_t* exp, uint32_t* out, size_t count, size_t k, int nb_rt, int bits, int w,
                           uint32_t* ws, uint32_t role, unsigned mask, const TmaMaps* maps = nullptr) {
     constexpr bool TILE = modexp_tiled(KLEV, TMA, NBT);
+    constexpr bool COOP = LANES > 1;
     using A = std::conditional_t<TILE, ArrT, Arr>;
     const int nb = NBT ? NBT : nb_rt;  // compile-time block count for the hot sizes
     const int L = C * nb, Q4 = L / 4;
@@ -318,8 +319,8 @@ MPB_DEVI void modexp_body(const uint32_t* N, const uint32_t* NP, const uint32_t*
             const int pos = win * w, wi = pos >> 5, off = pos & 31;
             uint32_t v = word_at(exp, count, k, wi) >> off;
             if (off + w > 32 && wi + 1 < L) v |= word_at(exp, count, k, wi + 1) << (32 - off);
-            if constexpr (COOP) {  // the two lanes scan alternate chunk groups of every entry
-                ct_select<select_unroll<C>(), 4>(G, L, nent, v & ((1u << w) - 1u), O, (int)role, 2);
+            if constexpr (COOP) {  // the lanes of an operand scan alternate chunk groups of every entry
+                ct_select<select_unroll<C>(), 4>(G, L, nent, v & ((1u << w) - 1u), O, (int)role, LANES);
                 __syncwarp(mask);
             } else {
                 ct_select<select_unroll<C>(), select_group<C, TILE>()>(G, L, nent, v & ((1u << w) - 1u), O);
@@ -327,16 +328,18 @@ MPB_DEVI void modexp_body(const uint32_t* N, const uint32_t* NP, const uint32_t*
             continue;
         }
         if (RM != 2 && mode == MODE_REDC) {  // T = X zero-extended to 2L limbs (CIOS: MontMul(X, 1))
+            if (!COOP || role == 0) {  // one writer per operand
 #pragma unroll 1
-            for (int q = 0; q < Q4; q++) {
-                T.st(q, X.ld(q));
-                T.st(Q4 + q, make_uint4(0, 0, 0, 0));
+                for (int q = 0; q < Q4; q++) {
+                    T.st(q, X.ld(q));
+                    T.st(Q4 + q, make_uint4(0, 0, 0, 0));
+                }
             }
             if constexpr (COOP) __syncwarp(mask);
         }
         if constexpr (COOP) {
             static_assert(RM != 2 && KLEV == 0, "cooperative operands: truncated or full REDC, schoolbook");
-            mont_op_coop<C, RM == 1>(mode, nb, X, B, Nt, NPt, T, Q, O, sg, role, mask);
+            mont_op_coop<C, RM == 1, LANES>(mode, nb, X, B, Nt, NPt, T, Q, O, sg, role, mask);
         } else if constexpr (TMA) {
             static_assert(RM != 2 && KLEV == 0, "TMA operand tiles: truncated or full REDC, schoolbook");
             mont_op<C, RM == 1, true>(mode, nb, X, B, Nt, NPt, Tt, Qt, O, sg, &tph);
@@ -361,8 +364,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_modexp(
     size_t k_ofs, size_t n_run, int nb_rt, int bits, int w, uint32_t* ws) {
     const size_t t = tid_global();
     if (t >= n_run) return;
-    modexp_body<C, RM, NBT, KLEV, false>(N, NP, R2, base, exp, out, count, k_ofs + t, nb_rt, bits, w, ws, 0u,
-                                         0xFFFFFFFFu);
+    modexp_body<C, RM, NBT, KLEV, 1>(N, NP, R2, base, exp, out, count, k_ofs + t, nb_rt, bits, w, ws, 0u,
+                                     0xFFFFFFFFu);
 }
 
 // One thread per operand, operand blocks loaded as per-warp TMA tiles (engine<.., TMA = true>).
@@ -373,25 +376,26 @@ __global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_modexp_tma(
     size_t k_ofs, size_t n_run, int nb_rt, int bits, int w, uint32_t* ws, const __grid_constant__ TmaMaps maps) {
     const size_t t = tid_global();
     if (t >= n_run) return;
-    modexp_body<C, RM, NBT, 0, false, true>(N, NP, R2, base, exp, out, count, k_ofs + t, nb_rt, bits, w, ws, 0u,
-                                            0xFFFFFFFFu, &maps);
+    modexp_body<C, RM, NBT, 0, 1, true>(N, NP, R2, base, exp, out, count, k_ofs + t, nb_rt, bits, w, ws, 0u,
+                                        0xFFFFFFFFu, &maps);
 }
 
-// Two lanes per operand (mp_coop.cuh): for >= 3072-bit batches whose cooperative launch fits one
-// CTA per SM (Launch::modexp).
-template <int C, int RM, int NBT>
+// LANES (2, 4, 8) lanes per operand (mp_coop.cuh): >= 3072-bit batches too small to fill the
+// GPU with one thread per operand, and the tail of a batch after its whole waves (Launch::modexp).
+template <int C, int RM, int NBT, int LANES>
 __global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_modexp_coop(
     const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP, const uint32_t* __restrict__ R2,
     const uint32_t* __restrict__ base, const uint32_t* __restrict__ exp, uint32_t* __restrict__ out, size_t count,
     size_t k_ofs, size_t n_run, int nb_rt, int bits, int w, uint32_t* ws) {
+    static_assert(LANES == 2 || LANES == 4 || LANES == 8, "lanes per operand");
     const size_t t = tid_global();
-    if ((t >> 1) >= n_run) return;
-    // lanes of this warp that own an operand: pairs are never split (2 * n_run is even)
+    if (t / LANES >= n_run) return;
+    // lanes of this warp that own an operand: groups are never split (32 % LANES == 0)
     const size_t wbase = t & ~(size_t)31;
-    const size_t lanes = 2 * n_run - wbase;
+    const size_t lanes = LANES * n_run - wbase;
     const unsigned mask = lanes >= 32 ? 0xFFFFFFFFu : ((1u << lanes) - 1u);
-    modexp_body<C, RM, NBT, 0, true>(N, NP, R2, base, exp, out, count, k_ofs + (t >> 1), nb_rt, bits, w, ws,
-                                     (uint32_t)(t & 1), mask);
+    modexp_body<C, RM, NBT, 0, LANES>(N, NP, R2, base, exp, out, count, k_ofs + t / LANES, nb_rt, bits, w, ws,
+                                      (uint32_t)(t % LANES), mask);
 }
 
 // ------------------------------------------------------------------- setup
@@ -671,9 +675,20 @@ inline int tma_policy() {
     }();
     return v;
 }
+// MPB_COOP: unset = the measured policy; 0 = always one thread per operand; 1 or 2 / 4 / 8 =
+// always 2 / 2 / 4 / 8 lanes per operand (tests and tuning)
 inline int coop_policy() {
     static int v = [] {
         const char* e = getenv("MPB_COOP");
+        return e ? atoi(e) : -1;
+    }();
+    return v;
+}
+// MPB_COOP_TAIL: lanes per operand of the tail after whole waves and of sub-wave batches
+// (unset = the measured policy; 0 = no cooperative tail / no 4- and 8-lane launches)
+inline int coop_tail_lanes() {
+    static int v = [] {
+        const char* e = getenv("MPB_COOP_TAIL");
         return e ? atoi(e) : -1;
     }();
     return v;
@@ -709,18 +724,24 @@ void Launch<C>::modexp(const uint32_t* N, const uint32_t* NP, const uint32_t* R2
             }
             go(std::integral_constant<int, 0>{});
         };
-        auto coop = [&](size_t k0, size_t n) {
+        auto coop = [&](size_t k0, size_t n, int lanes) {
             if (n == 0) return;
-            const unsigned g = grid_for(2 * n);
-            if (redc == 1)
-                k_modexp_coop<C, 1, NBT><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, k0, n, nb, bits,
-                                                                window, ws);
-            else
-                k_modexp_coop<C, 0, NBT><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, k0, n, nb, bits,
-                                                                window, ws);
+            const unsigned g = grid_for((size_t)lanes * n);
+            auto go = [&](auto LC) {
+                constexpr int LN = decltype(LC)::value;
+                if (redc == 1)
+                    k_modexp_coop<C, 1, NBT, LN><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, k0, n, nb,
+                                                                        bits, window, ws);
+                else
+                    k_modexp_coop<C, 0, NBT, LN><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, k0, n, nb,
+                                                                        bits, window, ws);
+            };
+            if (lanes >= 8) go(std::integral_constant<int, 8>{});
+            else if (lanes == 4) go(std::integral_constant<int, 4>{});
+            else go(std::integral_constant<int, 2>{});
         };
         const int pol = coop_policy();
-        if (redc != 2 && levels == 0 && pol != 1 && tma_policy() == 1) {
+        if (redc != 2 && levels == 0 && pol <= 0 && tma_policy() == 1) {
             // opt-in (MPB_TMA=1): one thread per operand with per-warp TMA operand tiles -- correct,
             // but 10 % slower than the cp.async.ca stage, whose operand blocks re-hit in L1
             // (DESIGN.md 5.3); falls back when the tensor maps cannot be encoded
@@ -746,19 +767,24 @@ void Launch<C>::modexp(const uint32_t* N, const uint32_t* NP, const uint32_t* R2
             }
         }
         if (redc == 2 || levels > 0 || pol == 0) return single(0, count);
-        if (pol == 1) return coop(0, count);
-        // Measured: two lanes per operand pay for >= 3072-bit operands at low
-        // occupancy (1.23x at 4096 bits); at 1024/2048 bits or near half occupancy they do not.
+        if (pol == 1 || pol == 2 || pol == 4 || pol == 8) return coop(0, count, pol == 1 ? 2 : pol);  // forced
+        // Measured: cooperative lanes pay for >= 3072-bit operands at low occupancy;
+        // at 1024/2048 bits they do not.
         if (C * nb < 96) return single(0, count);
         int dev = 0, sms = 148;
         if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        // small batch: the cooperative launch still fits one CTA per SM (measured crossover: two
-        // lanes per operand win 1.19x at 4096 bits up to 9472 operands = 148 CTAs, and lose once
-        // SMs hold two cooperative CTAs, e.g. 638 vs 607 ms at 14208)
-        if (2 * count <= (size_t)sms * kThreads) return coop(0, count);
-        // (a cooperative tail after the whole waves measured neutral at 2^16 x 4096 bits: the
-        // one-thread tail already overlaps the drain of the last wave)
-        single(0, count);
+        const size_t wave = (size_t)sms * kThreads * min_blocks<C>();  // one-thread operands resident at once
+        const int tl = coop_tail_lanes();
+        // a batch below one wave: as many lanes per operand as keep the launch within one wave
+        if (count <= wave / 8 && tl != 0) return coop(0, count, 8);
+        if (count <= wave / 4 && tl != 0) return coop(0, count, 4);
+        if (2 * count <= (size_t)sms * kThreads) return coop(0, count, 2);
+        // whole waves one thread per operand, then the tail (< one wave) with several lanes per
+        // operand so that it fills the SMs instead of running a few warps per SM
+        const size_t full = count / wave * wave, rest = count - full;
+        if (full == 0 || rest == 0 || tl == 0) return single(0, count);
+        single(0, full);
+        coop(full, rest, tl > 0 ? tl : (rest * 4 <= wave ? 4 : 2));
     });
 }
 

@@ -41,6 +41,14 @@ struct Launch {
 MPB_BLOCKS(MPB_EXTERN)
 #undef MPB_EXTERN
 
+// radix-2^52 FP64 exponentiation (inst_D52.cu, mp_dfma.cuh): digits D for a size (0 = unsupported),
+// its workspace, and the launch (false if the size is unsupported)
+int d52_digits(int bits);
+size_t d52_workspace_bytes(size_t count, int bits, int window);
+bool launch_modexp_d52(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
+                       const uint32_t* exp, uint32_t* out, size_t count, int bits, int window, bool trunc,
+                       uint32_t* ws, cudaStream_t s);
+
 // scratch blocks of the Karatsuba product (mirror of mp_kara.cuh kara_scratch_blocks)
 inline int kara_scratch_blocks_host(int nb, int level) {
     return level <= 0 || nb < 2 ? 0 : 4 * ((nb + 1) / 2) + kara_scratch_blocks_host((nb + 1) / 2, level - 1);

@@ -18,19 +18,33 @@
 
 namespace mpb {
 
-// W (2C+1 words) += the partner lane's W: both lanes end with the same sum.
-template <int C>
+// W (2C+1 words) = the sum of the G lanes' windows (butterfly over lanes xor 1, 2, .., G/2): every
+// lane of the group ends with the same total.  Partial sums never exceed the total (all terms are
+// non-negative parts of one column sum), so the window cannot overflow.
+template <int C, int G>
 MPB_DEVI void coop_window_sum(uint32_t (&W)[2 * C + 1], unsigned mask) {
-    uint32_t o[2 * C + 1];
 #pragma unroll
-    for (int i = 0; i <= 2 * C; i++) o[i] = __shfl_xor_sync(mask, W[i], 1);
-    add_first(W[0], o[0]);
+    for (int m = 1; m < G; m <<= 1) {
+        uint32_t o[2 * C + 1];
 #pragma unroll
-    for (int i = 1; i < 2 * C; i++) add_next(W[i], o[i]);
-    add_end(W[2 * C], o[2 * C]);
+        for (int i = 0; i <= 2 * C; i++) o[i] = __shfl_xor_sync(mask, W[i], m);
+        add_first(W[0], o[0]);
+#pragma unroll
+        for (int i = 1; i < 2 * C; i++) add_next(W[i], o[i]);
+        add_end(W[2 * C], o[2 * C]);
+    }
+}
+template <int G>
+MPB_DEVI uint32_t coop_or(uint32_t v, unsigned mask) {
+#pragma unroll
+    for (int m = 1; m < G; m <<= 1) v |= __shfl_xor_sync(mask, v, m);
+    return v;
 }
 
-template <int C, bool TRUNC, class AR = Arr>
+// G lanes per operand (G = 2, 4, 8): role r in [0, G) takes the pairs s = s_lo + G*i + r of each
+// block column; role 0 alone carries the column's carry-in, stores, and reads T blocks the phase
+// rewrites (see the invariant at the column end).
+template <int C, bool TRUNC, int G = 2, class AR = Arr>
 MPB_DEVI void engine_coop(int ph, int NB, const AR& AX, const AR& AY, const AR& DST, const AR& T, const AR& N,
                           const AR& OUT, uint32_t& orlo, uint32_t& tl1, const Stage& sg, uint32_t role,
                           unsigned mask) {
@@ -71,7 +85,7 @@ MPB_DEVI void engine_coop(int ph, int NB, const AR& AX, const AR& AY, const AR& 
     auto s_hi_of = [&](int k) { return sqr ? ((k - 1) >> 1) : (k < NB - 1 ? k : NB - 1); };
     auto iters_of = [&](int k) {
         const int n = s_hi_of(k) - s_lo_of(k) + 1;
-        return (n > 0 ? (n + 1) >> 1 : 0) + ((sqr && !(k & 1)) ? 1 : 0);
+        return (n > 0 ? (n + G - 1) / G : 0) + ((sqr && !(k & 1)) ? 1 : 0);
     };
     // this role's pair in iteration it of column k: s (a valid block index), valid, diagonal
     auto pair_of = [&](int k, int it, int& s, bool& valid, bool& diag) {
@@ -80,7 +94,7 @@ MPB_DEVI void engine_coop(int ph, int NB, const AR& AX, const AR& AY, const AR& 
             s = k >> 1;
             valid = role == 0;
         } else {
-            s = s_lo_of(k) + 2 * it + (int)role;
+            s = s_lo_of(k) + G * it + (int)role;
             valid = s <= s_hi_of(k);
             if (!valid) s = s_lo_of(k);
         }
@@ -181,7 +195,7 @@ MPB_DEVI void engine_coop(int ph, int NB, const AR& AX, const AR& AY, const AR& 
             // Invariant: only role 0 stores (DST, T, OUT) and only role 0 reads T blocks that this
             // phase rewrites; role 1's column results are discarded (its window is cleared below)
             // and the phase ends with __syncwarp, so no lane reads a block the other is storing.
-            coop_window_sum<C>(W, mask);
+            coop_window_sum<C, G>(W, mask);
             if (ph != PH_HI) {
                 if (role == 0) stb<C>(DST, k, W);
                 w_shift<C>(W);
@@ -222,12 +236,12 @@ MPB_DEVI void engine_coop(int ph, int NB, const AR& AX, const AR& AY, const AR& 
         k = nk;
         it = nit;
     }
-    // the top of the walk: role 1's window is zero, role 0 holds it; make both hold it
-    coop_window_sum<C>(W, mask);
+    // the top of the walk: only role 0's window is non-zero; make every lane hold it
+    coop_window_sum<C, G>(W, mask);
     if ((ph == PH_MUL || ph == PH_SQR) && role == 0) stb<C>(DST, 2 * NB - 1, W);
-    if (ph == PH_Q) {  // both roles need c_add / the correction inputs
-        orlo |= __shfl_xor_sync(mask, orlo, 1);
-        tl1 |= __shfl_xor_sync(mask, tl1, 1);
+    if (ph == PH_Q) {  // every role needs c_add / the correction inputs
+        orlo = coop_or<G>(orlo, mask);
+        tl1 = coop_or<G>(tl1, mask);
     }
     if (ph == PH_HI) {
         if (TRUNC) {
@@ -251,7 +265,7 @@ MPB_DEVI void engine_coop(int ph, int NB, const AR& AX, const AR& AY, const AR& 
     __syncwarp(mask);  // both lanes' stores are visible to both before the next phase
 }
 
-template <int C, bool TRUNC, class AR = Arr>
+template <int C, bool TRUNC, int G = 2, class AR = Arr>
 MPB_DEVI void mont_op_coop(int mode, int NB, const AR& X, const AR& B, const AR& N, const AR& NP, const AR& T,
                            const AR& Q, const AR& OUT, const Stage& sg, uint32_t role, unsigned mask) {
     uint32_t orlo = 0, tl1 = 0;
@@ -261,7 +275,7 @@ MPB_DEVI void mont_op_coop(int mode, int NB, const AR& X, const AR& B, const AR&
         const AR ax = step == 0 ? X : (step == 1 ? T : Q);
         const AR ay = step == 0 ? B : (step == 1 ? NP : N);
         const AR dst = step == 0 ? T : Q;
-        engine_coop<C, TRUNC>(ph, NB, ax, ay, dst, T, N, OUT, orlo, tl1, sg, role, mask);
+        engine_coop<C, TRUNC, G>(ph, NB, ax, ay, dst, T, N, OUT, orlo, tl1, sg, role, mask);
     }
 }
 

@@ -55,6 +55,9 @@ def test_host_only_helpers(lib):
     assert lib.mont_batch_modexp_ct_workspace(10, 2048, 5, 0) == 32 * 64 * (32 + 7) * 4
     assert lib.mont_batch_modexp_ct_workspace(64, 2048, 5, 0) == 64 * 64 * (32 + 7) * 4
     assert lib.mont_batch_modexp_ct_workspace(10, 2048, 7, 0) == 0
+    # radix-2^52 path (algo 4): D = 40 digits at 2048 bits as doubles, 2^w + 8 numbers per operand
+    assert lib.mont_batch_modexp_ct_workspace(10, 2048, 5, 4) == 32 * 20 * 16 * (32 + 8)
+    assert lib.mont_batch_modexp_ct_workspace(10, 700, 5, 4) == 0  # no radix-2^52 instance
     lib.mont_batch_setup_workspace.restype = ctypes.c_size_t
     lib.mont_batch_setup_workspace.argtypes = [ctypes.c_size_t, ctypes.c_int]
     assert lib.mont_batch_setup_workspace(10, 2048) == 10 * 6 * 64 * 4
@@ -110,6 +113,14 @@ def test_host_side_argument_checks(lib):
     assert lib.mont_batch_modexp_ct(None, None, None, None, None, None, 4, 1024, 5, 1, 9, None, 0, None) == EINVAL
     assert lib.mont_batch_modexp_ct(None, None, None, None, None, None, big, 1024, 5, 1, 0, None, 0, None) \
         == EUNSUPPORTED
+    # radix-2^52 exponentiation: truncated / full REDC only, sizes with an instance only, not a product
+    assert lib.mont_batch_modexp_ct(None, None, None, None, None, None, 4, 2048, 5, 2, 4, None, 0, None) \
+        == EUNSUPPORTED
+    assert lib.mont_batch_modexp_ct(None, None, None, None, None, None, 4, 700, 5, 1, 4, None, 0, None) \
+        == EUNSUPPORTED
+    assert lib.mont_batch_modexp_ct(None, None, None, None, None, None, 4, 2048, 5, 1, 5, None, 0, None) == EINVAL
+    lib.mp_batch_mul.argtypes = [vp, vp, vp, sz, i, i, vp, sz, vp]
+    assert lib.mp_batch_mul(None, None, None, 4, 2048, 4, None, 0, None) == EUNSUPPORTED
     # CRT-RSA runs 2 * count half-size operands in one exponentiation: at most 2^26 per call
     lib.rsa_batch_crt_ct.argtypes = [vp, vp, vp, vp, vp, vp, vp, sz, i, i, i, vp, sz, vp]
     crt_big = (1 << 26) + 1

@@ -152,12 +152,15 @@ def test_mont_redc_adversarial(mpb, bits, redc):
 
 def _gamma_low(rng: random.Random, N: int, L: int, k: int) -> int:
     """A gamma-family T (forced wrap of column L-1, tests/adversarial.py) with a zero high half
-    and T < N, so it is a valid operand in the R^2 position of the exponentiation."""
+    and T < N, so it is a valid operand in the R^2 position of the exponentiation.  The forced wrap
+    makes word L-1 of q*N mod R tiny, so T = -q*N mod R has its top word near 2^32 - 1: N needs an
+    all-ones top word (the caller crafts such moduli)."""
     R = 1 << (32 * L)
-    while True:
+    for _ in range(1000):
         t = t_gamma(rng, N, L, k) % R
         if t < N:
             return t
+    raise AssertionError("no gamma-family T below N (the modulus needs an all-ones top word)")
 
 
 def _schedule_modexp(base: int, e: int, N: int, rho: int, L: int, bits: int, w: int) -> int:
@@ -213,9 +216,10 @@ def test_theorem2_correction_fires_in_shipped_modexp_kernel(mpb):
     L = I.limbs_for_bits(bits)
     R = 1 << (32 * L)
     N, base, exp = I.modexp_inputs(config=3, count=count, bits=bits, dataset=7)
+    crafted = list(range(0, count, 2))  # even operands crafted, odd ones keep R^2 mod N
+    N[crafted, L - 1] = np.uint32(0xFFFFFFFF)  # raises N only: bases stay below it
     Ns, Bs, Es = ints(N), ints(base), ints(exp)
     rng = random.Random(2410)
-    crafted = list(range(0, count, 2))  # even operands crafted, odd ones keep R^2 mod N
     rho = [(_gamma_low(rng, n, L, k % 3) if k in crafted else R * R % n) for k, n in enumerate(Ns)]
     assert _schedule_modexp(Bs[1], Es[1], Ns[1], rho[1], L, bits, w) == pow(Bs[1], Es[1], Ns[1])
     dN, dB, dE = (mpb.to_device(x) for x in (N, base, exp))
@@ -331,6 +335,72 @@ def test_modexp_host_e2e(mpb):
     N, base, exp = I.modexp_inputs(config=5, count=count, bits=bits)
     out = mpb.modexp_host(N, base, exp, bits, window=5)
     assert np.array_equal(out, O.batch_modexp(base, exp, bits, N))
+
+
+# ------------------------------------------------- radix-2^52 FP64 path (f3)
+BITS_D52 = [1024, 2048, 3072, 4096, 4108]
+D52_COUNTS = {1024: 40, 2048: 37, 3072: 5, 4096: 3, 4108: 3}
+
+
+@pytest.mark.parametrize("redc", REDC_STANDALONE)
+@pytest.mark.parametrize("bits", BITS_D52)
+def test_modexp_radix52(mpb, bits, redc):
+    """mont_batch_modexp_ct with algo = RADIX52 (52-bit limbs on the FP64 pipe, mp_dfma.cuh) against
+    the oracle, truncated and full REDC, ragged counts (partial warp tiles / CTAs)."""
+    count = D52_COUNTS[bits]
+    N, base, exp = I.modexp_inputs(config=3, count=count, bits=bits, dataset=52)
+    dN = mpb.to_device(N)
+    Np, R2 = mpb.mont_batch_setup(dN, bits)
+    out = mpb.to_host(mpb.mont_batch_modexp_ct(dN, Np, R2, mpb.to_device(base), mpb.to_device(exp), bits,
+                                               window=5, redc=redc, algo=mpb.ALGO_RADIX52))
+    assert np.array_equal(out, O.batch_modexp(base, exp, bits, N))
+
+
+@pytest.mark.parametrize("window", [1, 2, 3, 4, 5, 6])
+def test_modexp_radix52_window_independence(mpb, window):
+    bits, count = 2048, 9
+    N, base, exp = I.modexp_inputs(config=1, count=count, bits=bits, dataset=window)
+    dN = mpb.to_device(N)
+    Np, R2 = mpb.mont_batch_setup(dN, bits)
+    out = mpb.to_host(mpb.mont_batch_modexp_ct(dN, Np, R2, mpb.to_device(base), mpb.to_device(exp), bits,
+                                               window=window, algo=mpb.ALGO_RADIX52))
+    assert np.array_equal(out, O.batch_modexp(base, exp, bits, N))
+
+
+def test_modexp_radix52_special_operands(mpb):
+    """Edge operands through the radix-2^52 path: 0^0, base 0, base 1, base N-1 (even / odd
+    exponents), all-ones exponent, exponent 1, 2^(bits-1), moduli with all-ones limbs."""
+    bits = 2048
+    L = I.limbs_for_bits(bits)
+    N, base, exp = I.modexp_inputs(config=1, count=12, bits=bits, dataset=3)
+    N[10] = np.uint32(0xFFFFFFFF)  # N = 2^2048 - 1 (odd, all ones)
+    N[11] = 0
+    N[11, 0] = 1
+    N[11, L - 1] = np.uint32(1 << 31)  # N = 2^2047 + 1
+    Ns = ints(N)
+    cases = [(0, 0), (0, 5), (1, 123), (Ns[3] - 1, 1 << 20), (Ns[4] - 1, (1 << 20) + 1), (7, (1 << bits) - 1),
+             (Ns[6] - 2, 1), (3, 1 << (bits - 1)), (Ns[8] // 2, 65537), (2, Ns[9] - 1), (Ns[10] - 1, 3),
+             (Ns[11] - 3, 12345678)]
+    for k, (bv, ev) in enumerate(cases):
+        base[k] = I.to_limbs(bv, L)
+        exp[k] = I.to_limbs(ev, L)
+    dN = mpb.to_device(N)
+    Np, R2 = mpb.mont_batch_setup(dN, bits)
+    for redc in REDC_STANDALONE:
+        out = mpb.to_host(mpb.mont_batch_modexp_ct(dN, Np, R2, mpb.to_device(base), mpb.to_device(exp), bits,
+                                                   redc=redc, algo=mpb.ALGO_RADIX52))
+        for k, (bv, ev) in enumerate(cases):
+            assert I.from_limbs(out[k]) == pow(bv, ev, Ns[k]), (redc, k)
+
+
+def test_modexp_radix52_rejects_unsupported(mpb):
+    bits = 700
+    N, base, exp = I.modexp_inputs(config=1, count=4, bits=bits)
+    dN = mpb.to_device(N)
+    Np, R2 = mpb.mont_batch_setup(dN, bits)
+    with pytest.raises(ValueError):
+        mpb.mont_batch_modexp_ct(dN, Np, R2, mpb.to_device(base), mpb.to_device(exp), bits,
+                                 algo=mpb.ALGO_RADIX52)
 
 
 # -------------------------------------------------- full-size, sampled checks
@@ -605,12 +675,12 @@ for bits, count, w, redc in ((1024, 9, 5, 1), (2048, 5, 4, 0), (3072, 4, 5, 1), 
 """
 
 
-@pytest.mark.parametrize("coop", ["0", "1", "tma"])
+@pytest.mark.parametrize("coop", ["0", "1", "4", "8", "tma"])
 def test_modexp_one_thread_and_two_lane_kernels(mpb, coop):
-    """All three exponentiation kernels, forced by MPB_COOP / MPB_TMA in a subprocess (the policy is
-    read once per process): one thread per operand (0), two lanes per operand (1, mp_coop.cuh) and
-    one thread per operand with per-warp TMA operand tiles (tma), 1024..4108 bits, truncated and
-    full REDC, against the oracle."""
+    """All exponentiation kernels, forced by MPB_COOP / MPB_TMA in a subprocess (the policy is read
+    once per process): one thread per operand (0), two / four / eight lanes per operand (1, 4, 8:
+    mp_coop.cuh, shuffle-summed block-column windows) and one thread per operand with per-warp TMA
+    operand tiles (tma), 1024..4108 bits, truncated and full REDC, against the oracle."""
     import os
     import subprocess
     import sys
