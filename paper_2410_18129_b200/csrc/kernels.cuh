@@ -775,16 +775,18 @@ void Launch<C>::modexp(const uint32_t* N, const uint32_t* NP, const uint32_t* R2
         if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const size_t wave = (size_t)sms * kThreads * min_blocks<C>();  // one-thread operands resident at once
         const int tl = coop_tail_lanes();
-        // a batch below one wave: as many lanes per operand as keep the launch within one wave
-        if (count <= wave / 8 && tl != 0) return coop(0, count, 8);
-        if (count <= wave / 4 && tl != 0) return coop(0, count, 4);
+        // (opt-in, MPB_COOP_TAIL = 4 / 8) sub-wave batches with 4 or 8 lanes per operand
+        if (tl >= 8 && count <= wave / 8) return coop(0, count, 8);
+        if (tl >= 4 && count <= wave / 4) return coop(0, count, 4);
         if (2 * count <= (size_t)sms * kThreads) return coop(0, count, 2);
-        // whole waves one thread per operand, then the tail (< one wave) with several lanes per
-        // operand so that it fills the SMs instead of running a few warps per SM
+        // (opt-in, MPB_COOP_TAIL = 2 / 4 / 8) whole waves one thread per operand, then the tail with
+        // several lanes per operand.  Measured at 2^16 x 4096 bits: 41.9 K/s without,
+        // 39.6 / 40.3 / 31.8 K/s with a 2 / 4 / 8-lane tail -- the one-thread tail, which starts as the
+        // last whole wave drains and runs a few warps per SM, is faster; so it stays the default.
         const size_t full = count / wave * wave, rest = count - full;
-        if (full == 0 || rest == 0 || tl == 0) return single(0, count);
+        if (tl <= 1 || full == 0 || rest == 0) return single(0, count);
         single(0, full);
-        coop(full, rest, tl > 0 ? tl : (rest * 4 <= wave ? 4 : 2));
+        coop(full, rest, tl);
     });
 }
 

@@ -403,6 +403,35 @@ def test_modexp_radix52_rejects_unsupported(mpb):
                                  algo=mpb.ALGO_RADIX52)
 
 
+def test_fault_injection_negative_control(mpb):
+    """Negative control of the parity harness: the comparison that passes on the kernel's
+    output must fail when one bit of one output limb is flipped -- in the element-wise oracle
+    comparison, in the truncated == full whole-batch comparison, and in the slicing-independent
+    digest config 5 prints."""
+    from paper_2410_18129_b200 import shard
+
+    bits, count = 1024, 33
+    N, base, exp = I.modexp_inputs(config=3, count=count, bits=bits, dataset=99)
+    dN = mpb.to_device(N)
+    Np, R2 = mpb.mont_batch_setup(dN, bits)
+    dB, dE = mpb.to_device(base), mpb.to_device(exp)
+    out_t = mpb.mont_batch_modexp_ct(dN, Np, R2, dB, dE, bits, 5, redc=1)
+    out_f = mpb.mont_batch_modexp_ct(dN, Np, R2, dB, dE, bits, 5, redc=0)
+    ref = O.batch_modexp(base, exp, bits, N)
+    h = mpb.to_host(out_t)
+    assert np.array_equal(h, ref) and torch.equal(out_t, out_f)
+    rng = np.random.default_rng(7)
+    for _ in range(8):
+        k, i, b = int(rng.integers(count)), int(rng.integers(h.shape[1])), int(rng.integers(32))
+        bad = h.copy()
+        bad[k, i] ^= np.uint32(1 << b)
+        assert not np.array_equal(bad, ref)
+        assert shard.digest_combine([shard.digest_part(bad, 0)]) != shard.digest_combine([shard.digest_part(ref, 0)])
+        flipped = out_t.clone()
+        flipped[i // 4, k, i % 4] ^= (1 << b) if b < 31 else -(1 << 31)
+        assert not torch.equal(flipped, out_f)
+
+
 # -------------------------------------------------- full-size, sampled checks
 @pytest.mark.slow
 def test_config3_full_batch_sampled(mpb):
