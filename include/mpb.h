@@ -50,14 +50,18 @@ enum { MPB_REDC_FULL = 0, MPB_REDC_TRUNCATED = 1, MPB_REDC_CIOS = 2 };
 /* AUTO = schoolbook: on sm_100a the blocked schoolbook engine beat every Karatsuba variant at every
  * measured size, so there is no crossover to select; KARATSUBA = one level,
  * KARATSUBA2 = two levels, explicit requests only. */
-enum { MPB_ALGO_AUTO = 0, MPB_ALGO_SCHOOLBOOK = 1, MPB_ALGO_KARATSUBA = 2, MPB_ALGO_KARATSUBA2 = 3, MPB_ALGO_RADIX52 = 4 };
+enum { MPB_ALGO_AUTO = 0, MPB_ALGO_SCHOOLBOOK = 1, MPB_ALGO_KARATSUBA = 2, MPB_ALGO_KARATSUBA2 = 3, MPB_ALGO_RADIX52 = 4,
+       MPB_ALGO_HYBRID = 5 };
 /* RADIX52 (mont_batch_modexp_ct only): the exponentiation runs internally on 52-bit limbs held in
  * doubles, every word product split exactly into its low and high 52-bit halves by two FP64 fused
  * multiply-adds (the paper's own radix and madd52lo/hi) and summed without carries;
  * Montgomery reduction modulo 2^(52D) with truncated or full REDC (not CIOS).  Same inputs (the
  * 32-bit N', R^2 mod N: the 52-bit constants are derived in the kernel), same canonical result.
  * Sizes: bits with a D in {20, 40, 64, 80} such that 52D >= bits + 2 and 0 <= 130D - 64L <= bits - 2
- * (1024, 2048, 3072, 4096 and 4108 bits among them); other sizes MPB_EUNSUPPORTED. */
+ * (1024, 2048, 3072, 4096 and 4108 bits among them); other sizes MPB_EUNSUPPORTED.
+ * HYBRID (mont_batch_modexp_ct, 1921..2048 bits): one launch whose CTAs run either the 32-bit
+ * schoolbook exponentiation or the RADIX52 one on disjoint operand ranges, so the integer-multiply
+ * and FP64 pipes of an SM work at the same time; truncated or full REDC. */
 
 /* L(bits) = 4*ceil(bits/128); 0 if bits <= 0. */
 int mpb_limbs(int bits);

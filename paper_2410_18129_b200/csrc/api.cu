@@ -196,9 +196,9 @@ size_t mp_batch_workspace(size_t count, int bits, int algo) {
 static int mp_product(const uint32_t* a, const uint32_t* b, uint32_t* c, size_t count, int bits, int algo, bool sqr,
                       void* ws, size_t ws_bytes, void* stream) {
     g_err.clear();
-    if (algo < MPB_ALGO_AUTO || algo > MPB_ALGO_RADIX52) return fail(MPB_EINVAL, "algo out of range");
-    if (algo == MPB_ALGO_RADIX52)
-        return fail(MPB_EUNSUPPORTED, "MPB_ALGO_RADIX52 is an exponentiation path (mont_batch_modexp_ct)");
+    if (algo < MPB_ALGO_AUTO || algo > MPB_ALGO_HYBRID) return fail(MPB_EINVAL, "algo out of range");
+    if (algo >= MPB_ALGO_RADIX52)
+        return fail(MPB_EUNSUPPORTED, "MPB_ALGO_RADIX52 / HYBRID are exponentiation paths (mont_batch_modexp_ct)");
     int L;
     if (int rc = limbs_checked(bits, L)) return rc;
     if (count == 0) return MPB_OK;
@@ -289,6 +289,7 @@ size_t mont_batch_modexp_ct_workspace(size_t count, int bits, int window, int al
     const int L = mpb_limbs(bits);
     if (L <= 0 || window < 1 || window > 6) return 0;
     if (algo == MPB_ALGO_RADIX52) return mpb::d52_workspace_bytes(count, bits, window);
+    if (algo == MPB_ALGO_HYBRID) return mpb::hybrid_workspace_bytes(count, bits, window);
     const int C = block_of(L);
     const size_t kara = (size_t)mpb::kara_scratch_blocks_host(L / C, kara_levels(algo, L)) * C;
     // word-sliced layout (Karatsuba products, TMA tiles): G | Y | T | Q | S | scratch, stride count;
@@ -303,13 +304,15 @@ int mont_batch_modexp_ct(const uint32_t* N, const uint32_t* NP, const uint32_t* 
                          void* ws, size_t ws_bytes, void* stream) {
     g_err.clear();
     if (!redc_ok(redc)) return fail(MPB_EINVAL, "redc out of range");
-    if (algo < MPB_ALGO_AUTO || algo > MPB_ALGO_RADIX52) return fail(MPB_EINVAL, "algo out of range");
+    if (algo < MPB_ALGO_AUTO || algo > MPB_ALGO_HYBRID) return fail(MPB_EINVAL, "algo out of range");
     if (window < 1 || window > 6) return fail(MPB_EINVAL, "window must be in 1..6");
     if (redc == MPB_REDC_CIOS && (algo == MPB_ALGO_KARATSUBA || algo == MPB_ALGO_KARATSUBA2))
         return fail(MPB_EUNSUPPORTED, "CIOS (alg:8BlockMontRed) interleaves rows of a schoolbook product; "
                                       "Karatsuba needs MPB_REDC_FULL or MPB_REDC_TRUNCATED");
-    if (algo == MPB_ALGO_RADIX52 && redc == MPB_REDC_CIOS)
-        return fail(MPB_EUNSUPPORTED, "the radix-2^52 path has truncated and full REDC only");
+    if ((algo == MPB_ALGO_RADIX52 || algo == MPB_ALGO_HYBRID) && redc == MPB_REDC_CIOS)
+        return fail(MPB_EUNSUPPORTED, "the radix-2^52 / hybrid paths have truncated and full REDC only");
+    if (algo == MPB_ALGO_HYBRID && !mpb::hybrid_workspace_bytes(1, bits, window))
+        return fail(MPB_EUNSUPPORTED, "the hybrid path serves 1921..2048-bit operands");
     if (algo == MPB_ALGO_RADIX52 && !mpb::d52_digits(bits))
         return fail(MPB_EUNSUPPORTED, "bits=" + std::to_string(bits) + " has no radix-2^52 instance");
     int L;
@@ -321,6 +324,11 @@ int mont_batch_modexp_ct(const uint32_t* N, const uint32_t* NP, const uint32_t* 
         return fail(MPB_EINVAL, "output aliases an input");
     if (ws_bytes < mont_batch_modexp_ct_workspace(count, bits, window, algo))
         return fail(MPB_EINVAL, "workspace too small");
+    if (algo == MPB_ALGO_HYBRID) {
+        mpb::launch_modexp_hybrid(N, NP, R2, base, exp, out, count, bits, window, redc == MPB_REDC_TRUNCATED,
+                                  (uint32_t*)ws, (cudaStream_t)stream);
+        return check_launch();
+    }
     if (algo == MPB_ALGO_RADIX52) {
         mpb::launch_modexp_d52(N, NP, R2, base, exp, out, count, bits, window, redc == MPB_REDC_TRUNCATED,
                                (uint32_t*)ws, (cudaStream_t)stream);

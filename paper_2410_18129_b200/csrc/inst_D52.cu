@@ -18,13 +18,10 @@ namespace mpb {
 // Workspace (warp tiles over count rounded up to 32, D/2 chunks of 16 bytes per number):
 //   G (2^w numbers) | Y | T (2 numbers) | Q | S | N | N' | X
 template <int C, int NB, bool TRUNC>
-__global__ void __launch_bounds__(kThreads, 3) k_modexp_d52(const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP,
-                                                          const uint32_t* __restrict__ R2, const uint32_t* __restrict__ base,
-                                                          const uint32_t* __restrict__ exp, uint32_t* __restrict__ out,
-                                                          size_t count, int L, int bits, int w, uint32_t* ws) {
+MPB_DEVI void modexp_d52_body(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
+                              const uint32_t* exp, uint32_t* out, size_t count, size_t k, int L, int bits, int w,
+                              uint32_t* ws) {
     namespace d = d52;
-    const size_t k = tid_global();
-    if (k >= count) return;
     constexpr int D = C * NB, QD = D / 2;
     const int nent = 1 << w;
     const size_t cpad = (count + 31) & ~(size_t)31;
@@ -115,6 +112,39 @@ __global__ void __launch_bounds__(kThreads, 3) k_modexp_d52(const uint32_t* __re
     d::to32<D>(X, L, arr(out, count, k));
 }
 
+template <int C, int NB, bool TRUNC>
+__global__ void __launch_bounds__(kThreads, 3) k_modexp_d52(const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP,
+                                                          const uint32_t* __restrict__ R2, const uint32_t* __restrict__ base,
+                                                          const uint32_t* __restrict__ exp, uint32_t* __restrict__ out,
+                                                          size_t count, int L, int bits, int w, uint32_t* ws) {
+    const size_t k = tid_global();
+    if (k >= count) return;
+    modexp_d52_body<C, NB, TRUNC>(N, NP, R2, base, exp, out, count, k, L, bits, w, ws);
+}
+
+// Hybrid (MPB_ALGO_HYBRID, 2048 bits): ONE kernel whose CTAs take either arithmetic -- in every
+// group of three consecutive CTAs, two run the 32-bit IMAD exponentiation (k_modexp<16, RM, 4, 0>'s
+// body, operands 0 .. n32-1) and one the radix-2^52 FP64 exponentiation (operands n32 .. count-1),
+// so an SM's three resident CTAs mix the two and the IMAD (fmaheavy) and FP64 pipes work at the
+// same time.  Same results operand by operand (each operand runs one complete, constant-time
+// exponentiation).  ws32: the 32-bit path's tiled workspace for `count`; ws52: the radix-2^52 one.
+template <int RM>
+__global__ void __launch_bounds__(kThreads, 3) k_modexp_hybrid(
+    const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP, const uint32_t* __restrict__ R2,
+    const uint32_t* __restrict__ base, const uint32_t* __restrict__ exp, uint32_t* __restrict__ out, size_t count,
+    size_t n32, int L, int bits, int w, uint32_t* ws32, uint32_t* ws52) {
+    const unsigned g = blockIdx.x / 3, r = blockIdx.x % 3;
+    if (r < 2) {
+        const size_t k = ((size_t)(2 * g + r)) * kThreads + threadIdx.x;
+        if (k >= n32) return;
+        modexp_body<16, RM, 4, 0, 1>(N, NP, R2, base, exp, out, count, k, 4, bits, w, ws32, 0u, 0xFFFFFFFFu);
+    } else {
+        const size_t k = n32 + (size_t)g * kThreads + threadIdx.x;
+        if (k >= count) return;
+        modexp_d52_body<8, 5, RM == 1>(N, NP, R2, base, exp, out, count, k, L, bits, w, ws52);
+    }
+}
+
 // (C, NB) instances: 1024 (4, 5) D = 20; 2048 (8, 5) D = 40; 3072 (8, 8) D = 64; 4096 / 4108 (8, 10) D = 80
 int d52_digits(int bits) {
     const int L = 4 * ((bits + 127) / 128);
@@ -130,6 +160,42 @@ size_t d52_workspace_bytes(size_t count, int bits, int window) {
     if (!D) return 0;
     const size_t cpad = (count + 31) & ~(size_t)31;
     return cpad * (size_t)(D / 2) * 16 * (size_t)((1 << window) + 8);
+}
+
+// 32-bit share of a hybrid launch: MPB_HYBRID_FRAC (0..1, tuning) or 2/3 (two of three CTAs)
+static double hybrid_frac32() {
+    static double v = [] {
+        const char* e = getenv("MPB_HYBRID_FRAC");
+        const double f = e ? atof(e) : 2.0 / 3.0;
+        return f > 0.0 && f < 1.0 ? f : 2.0 / 3.0;
+    }();
+    return v;
+}
+
+size_t hybrid_workspace_bytes(size_t count, int bits, int window) {
+    if (bits <= 1920 || bits > 2048) return 0;  // L = 64 limbs (NB = 4 of C = 16) and D = 40
+    const size_t cpad = (count + 31) & ~(size_t)31;
+    const size_t ws32 = cpad * 64 * (size_t)((1 << window) + 7) * 4;
+    return ws32 + d52_workspace_bytes(count, bits, window) + 256;
+}
+
+bool launch_modexp_hybrid(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
+                          const uint32_t* exp, uint32_t* out, size_t count, int bits, int window, bool trunc,
+                          uint32_t* ws, cudaStream_t s) {
+    if (!hybrid_workspace_bytes(count, bits, window) || d52_digits(bits) != 40) return false;
+    const size_t cpad = (count + 31) & ~(size_t)31;
+    uint32_t* ws32 = ws;
+    uint32_t* ws52 = ws + ((cpad * 64 * (size_t)((1 << window) + 7) + 63) & ~(size_t)63);
+    // 32-bit operands: a whole number of 128-thread CTAs
+    size_t n32 = (size_t)(hybrid_frac32() * (double)count) / kThreads * kThreads;
+    if (n32 > count) n32 = count;
+    const size_t c32 = (n32 + kThreads - 1) / kThreads, c52 = (count - n32 + kThreads - 1) / kThreads;
+    const size_t groups = ((c32 + 1) / 2 > c52 ? (c32 + 1) / 2 : c52);
+    const unsigned g = (unsigned)(3 * groups);
+    const size_t sm = (size_t)kThreads * 4 * 4 * 16 + (kThreads / 32) * 16;
+    if (trunc) k_modexp_hybrid<1><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, n32, 64, bits, window, ws32, ws52);
+    else k_modexp_hybrid<0><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, n32, 64, bits, window, ws32, ws52);
+    return true;
 }
 
 bool launch_modexp_d52(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,

@@ -49,6 +49,12 @@ bool launch_modexp_d52(const uint32_t* N, const uint32_t* NP, const uint32_t* R2
                        const uint32_t* exp, uint32_t* out, size_t count, int bits, int window, bool trunc,
                        uint32_t* ws, cudaStream_t s);
 
+// hybrid 2048-bit exponentiation: 32-bit IMAD CTAs and radix-2^52 FP64 CTAs in one launch
+size_t hybrid_workspace_bytes(size_t count, int bits, int window);
+bool launch_modexp_hybrid(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
+                          const uint32_t* exp, uint32_t* out, size_t count, int bits, int window, bool trunc,
+                          uint32_t* ws, cudaStream_t s);
+
 // scratch blocks of the Karatsuba product (mirror of mp_kara.cuh kara_scratch_blocks)
 inline int kara_scratch_blocks_host(int nb, int level) {
     return level <= 0 || nb < 2 ? 0 : 4 * ((nb + 1) / 2) + kara_scratch_blocks_host((nb + 1) / 2, level - 1);

@@ -56,7 +56,7 @@ for _name, (_res, _args) in _SIGS.items():
 
 MPB_OK, MPB_EINVAL, MPB_EUNSUPPORTED, MPB_ECUDA = 0, -1, -2, -3
 REDC_FULL, REDC_TRUNCATED, REDC_CIOS = 0, 1, 2
-ALGO_AUTO, ALGO_SCHOOLBOOK, ALGO_KARATSUBA, ALGO_KARATSUBA2, ALGO_RADIX52 = 0, 1, 2, 3, 4
+ALGO_AUTO, ALGO_SCHOOLBOOK, ALGO_KARATSUBA, ALGO_KARATSUBA2, ALGO_RADIX52, ALGO_HYBRID = 0, 1, 2, 3, 4, 5
 
 
 class MpbError(RuntimeError):

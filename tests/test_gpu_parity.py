@@ -393,6 +393,24 @@ def test_modexp_radix52_special_operands(mpb):
             assert I.from_limbs(out[k]) == pow(bv, ev, Ns[k]), (redc, k)
 
 
+@pytest.mark.parametrize("redc", REDC_STANDALONE)
+@pytest.mark.parametrize("count", [1, 129, 700])
+def test_modexp_hybrid(mpb, count, redc):
+    """MPB_ALGO_HYBRID: one launch, 32-bit IMAD CTAs and radix-2^52 FP64 CTAs on disjoint operand
+    ranges (counts below one CTA, across the split, and with several CTA groups); every operand
+    equals the 32-bit path's result and, on a sample, the oracle."""
+    bits = 2048
+    N, base, exp = I.modexp_inputs(config=3, count=count, bits=bits, dataset=count)
+    dN, dB, dE = (mpb.to_device(x) for x in (N, base, exp))
+    Np, R2 = mpb.mont_batch_setup(dN, bits)
+    out = mpb.mont_batch_modexp_ct(dN, Np, R2, dB, dE, bits, 5, redc=redc, algo=mpb.ALGO_HYBRID)
+    ref32 = mpb.mont_batch_modexp_ct(dN, Np, R2, dB, dE, bits, 5, redc=redc, algo=mpb.ALGO_SCHOOLBOOK)
+    assert torch.equal(out, ref32)
+    h = mpb.to_host(out)
+    idx = sorted({0, count // 3, count // 2, count - 1})
+    assert np.array_equal(h[idx], O.batch_modexp(base[idx], exp[idx], bits, N[idx]))
+
+
 def test_modexp_radix52_rejects_unsupported(mpb):
     bits = 700
     N, base, exp = I.modexp_inputs(config=1, count=4, bits=bits)
