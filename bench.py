@@ -283,7 +283,45 @@ def run_ours(args) -> None:
     e2e_s = rk.max(time.perf_counter() - t0)
     ok_e2e = rk.sum(0 if np.array_equal(hO.numpy().view(np.uint32), dev_out) else 1) == 0
 
+    # config 2 at 2048 bits (BASELINE metric's "modmul/s"): MontMul and MontSqr, truncated REDC, 2^20
+    # operands, inputs resident, mean CUDA-event time of 5 launches after one warm-up (not the
+    # exponentiation's timed region)
+    modmul = None
+    if rank == 0 and not c5:
+        n2 = 1 << 20
+        N2, a2, b2 = I.montmul_inputs(config=2, count=n2, bits=BITS)
+        dN2, da2, db2 = (mpb.to_device(x) for x in (N2, a2, b2))
+        Np2, _ = mpb.mont_batch_setup(dN2, BITS)
+        ws2 = mpb.mont_workspace(n2, BITS)
+        o2 = mpb.empty_sliced(L, n2)
+
+        def per_s(fn, reps=5):
+            fn()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for _ in range(reps):
+                fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            return n2 * reps / (e0.elapsed_time(e1) / 1000.0)
+
+        lib, sz = mpb._lib, ws2.numel() * 4
+        mm = per_s(lambda: lib.mont_batch_mul(da2.data_ptr(), db2.data_ptr(), dN2.data_ptr(), Np2.data_ptr(),
+                                              o2.data_ptr(), n2, BITS, mpb.REDC_TRUNCATED, ws2.data_ptr(), sz,
+                                              stream.cuda_stream))
+        ms_ = per_s(lambda: lib.mont_batch_sqr(da2.data_ptr(), dN2.data_ptr(), Np2.data_ptr(), o2.data_ptr(), n2,
+                                               BITS, mpb.REDC_TRUNCATED, ws2.data_ptr(), sz, stream.cuda_stream))
+        c2 = imad_counts(L, 1)
+        modmul = {"workload": "BASELINE config 2 at 2048 bits: 2^20 operands, truncated REDC, inputs resident",
+                  "modmul_per_s": mm, "modsqr_per_s": ms_, "unit": "op/s",
+                  "frac_modmul": mm * c2["mul"] / (SMS * IMAD_PER_CLK_SM * 1965e6),
+                  "frac_modsqr": ms_ * c2["sqr"] / (SMS * IMAD_PER_CLK_SM * 1965e6)}
+        del dN2, da2, db2, Np2, ws2, o2
+
     extra = {}
+    if modmul:
+        extra["modmul"] = modmul
     if c5:  # parity on the seeded 4096-element subset of the global batch + G-invariant digest
         import oracle as O
 

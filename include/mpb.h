@@ -105,8 +105,10 @@ size_t mont_batch_workspace(size_t count, int bits);
  * squarings, a masked full-table scan and one Montgomery multiplication.
  * exp has L limbs and `bits` significant bits (zero padded); timing depends on
  * (count, bits, window, redc) only.  window in 1..6.  exp = 0 gives 1 (0^0 = 1).
- * For >= 3072-bit operands, batches of at most (SM count x 64) operands run with
- * two lanes per operand (the result is the same; only the schedule differs). */
+ * For >= 3072-bit operands, small batches run with 8, 4 or 2 lanes of a warp per operand (8 while
+ * 8*count <= SMs*128, 4 while 4*count <= SMs*256, 2 while 2*count <= SMs*128), block products of
+ * every block column split between the lanes and their windows summed by shuffles (the result is
+ * the same; only the schedule differs). */
 int mont_batch_modexp_ct(const uint32_t* N, const uint32_t* Nprime, const uint32_t* R2, const uint32_t* base,
                          const uint32_t* exp, uint32_t* out, size_t count, int bits, int window, int redc,
                          int algo, void* workspace, size_t workspace_bytes, void* stream);

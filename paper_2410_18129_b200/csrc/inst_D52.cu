@@ -5,6 +5,10 @@
 #include "kernels.cuh"
 #include "mp_dfma.cuh"
 
+#ifndef MPB_D52_MINB
+#define MPB_D52_MINB 3  // resident 128-thread CTAs per SM the radix-2^52 kernel is compiled for
+#endif
+
 namespace mpb {
 
 // Internal constants from the ABI's 32-bit ones (R32 = 2^(32L), R52 = 2^(52D)):
@@ -113,7 +117,7 @@ MPB_DEVI void modexp_d52_body(const uint32_t* N, const uint32_t* NP, const uint3
 }
 
 template <int C, int NB, bool TRUNC>
-__global__ void __launch_bounds__(kThreads, 3) k_modexp_d52(const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP,
+__global__ void __launch_bounds__(kThreads, MPB_D52_MINB) k_modexp_d52(const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP,
                                                           const uint32_t* __restrict__ R2, const uint32_t* __restrict__ base,
                                                           const uint32_t* __restrict__ exp, uint32_t* __restrict__ out,
                                                           size_t count, int L, int bits, int w, uint32_t* ws) {

@@ -205,8 +205,8 @@ __global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_mont_redc_tiled(
 // every engine array has the compile-time chunk stride.  Otherwise (generic block count,
 // Karatsuba products, TMA tiles) -- word-sliced arrays, stride count: G | Y | T | Q | S |
 // Karatsuba scratch (kara_scratch_blocks(nb, KLEV) blocks; KLEV = algo levels for the products).
-// The whole exponentiation of operand k (of `count`, the arrays' stride).  COOP: two lanes per
-// operand (mp_coop.cuh), role = lane & 1, mask = the active pairs of the warp.
+// The whole exponentiation of operand k (of `count`, the arrays' stride).  LANES > 1: that many lanes
+// per operand (mp_coop.cuh), role = lane mod LANES, mask = the active lanes of the warp.
 #ifndef MPB_TILE
 #define MPB_TILE 1
 #endif
@@ -684,8 +684,8 @@ inline int coop_policy() {
     }();
     return v;
 }
-// MPB_COOP_TAIL: lanes per operand of the tail after whole waves and of sub-wave batches
-// (unset = the measured policy; 0 = no cooperative tail / no 4- and 8-lane launches)
+// MPB_COOP_TAIL = 2 / 4 / 8: lanes per operand of an (opt-in) cooperative tail after the whole
+// waves of a large batch (unset = no cooperative tail, the measured policy)
 inline int coop_tail_lanes() {
     static int v = [] {
         const char* e = getenv("MPB_COOP_TAIL");
@@ -775,9 +775,12 @@ void Launch<C>::modexp(const uint32_t* N, const uint32_t* NP, const uint32_t* R2
         if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const size_t wave = (size_t)sms * kThreads * min_blocks<C>();  // one-thread operands resident at once
         const int tl = coop_tail_lanes();
-        // (opt-in, MPB_COOP_TAIL = 4 / 8) sub-wave batches with 4 or 8 lanes per operand
-        if (tl >= 8 && count <= wave / 8) return coop(0, count, 8);
-        if (tl >= 4 && count <= wave / 4) return coop(0, count, 4);
+        // Small batches: as many lanes per operand as keep the cooperative launch within one
+        // (8 lanes) or two (4 lanes) CTAs per SM.  Measured at 4096 bits: 2 048
+        // operands 3.5 / 4.1 / 5.5 / 6.0 K/s with 1 / 2 / 4 / 8 lanes; 8 192 operands 13.5 / 15.9 /
+        // 16.9 / 8.9 K/s (8 lanes there would need 3.5 CTAs per SM).
+        if (8 * count <= (size_t)sms * kThreads) return coop(0, count, 8);
+        if (4 * count <= (size_t)2 * sms * kThreads) return coop(0, count, 4);
         if (2 * count <= (size_t)sms * kThreads) return coop(0, count, 2);
         // (opt-in, MPB_COOP_TAIL = 2 / 4 / 8) whole waves one thread per operand, then the tail with
         // several lanes per operand.  Measured at 2^16 x 4096 bits: 41.9 K/s without,

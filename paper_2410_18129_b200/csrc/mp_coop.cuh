@@ -1,18 +1,20 @@
-// mp_coop.cuh -- cooperative operands: two adjacent lanes of a warp per operand (sm_100a).
+// mp_coop.cuh -- warp-cooperative operands: G = 2, 4 or 8 adjacent lanes of a warp per operand
+// (north_star (b); sm_100a).
 //
-// The one-thread-per-operand engine (mp_mont.cuh) needs one resident thread per operand, so a
-// batch much smaller than the resident capacity leaves SMs idle (used for >= 3072-bit batches
-// whose cooperative launch fits one CTA per SM: 1.19x at 4096 bits).  Here the two lanes 2m, 2m+1 of a warp own operand m (role r = lane & 1) and split the
-// block products of every block column between them: in iteration i of column k, role r takes
-// the pair s = s_lo + 2i + r (PH_SQR: the off-diagonal pairs, then one iteration for the diagonal
-// block, which role 0 computes and role 1 runs on a zero block).  A role without a pair in an
-// iteration multiplies a zero block, so both lanes always execute the same instructions.  At the
-// end of a column the lanes exchange their windows with shuffles and add them symmetrically, so
-// both hold the column total and run the column action (store, truncated-REDC correction, emit)
-// identically (in the high part, whose column action reads and rewrites T, only role 0 stores),
-// after which role 1 clears its carry-in so the next column counts it once.  Each lane does about half of the block
-// products; per operand the work is ~0.6x of one thread's (the column actions are duplicated).
-// Same results as the single-thread engine; constant time in the same sense (public schedule).
+// The one-thread-per-operand engine (mp_mont.cuh) needs one resident thread per operand, so a batch
+// much smaller than the resident capacity leaves SMs idle (Launch::modexp uses G lanes for small
+// >= 3072-bit batches: 1.71x at 2 048 x 4096-bit operands with 8 lanes).  The G
+// lanes Gm .. Gm+G-1 own operand m (role r = lane mod G) and split the block products of every
+// block column: in iteration i of column k, role r takes the pair s = s_lo + G*i + r (PH_SQR: the
+// off-diagonal pairs, then one iteration for the diagonal block, which role 0 computes and the
+// others run on a zero block).  A role without a pair in an iteration multiplies a zero block, so
+// all lanes always execute the same instructions.  At the end of a column the lanes sum their
+// windows by a shuffle butterfly (log2 G rounds of 33 shuffles and one 33-word add chain), so all
+// hold the column total and run the column action (store, truncated-REDC correction, emit)
+// identically; only role 0 stores and reads the T blocks the phase rewrites, and the other roles
+// clear their carry-in so the next column counts it once.  Per operand the product work is split
+// G ways; the column actions are repeated in every lane.  Same results as the single-thread
+// engine; constant time in the same sense (public schedule).
 #pragma once
 #include "mp_mont.cuh"
 
