@@ -8,6 +8,9 @@
 #ifndef MPB_D52_MINB
 #define MPB_D52_MINB 3  // resident 128-thread CTAs per SM the radix-2^52 kernel is compiled for
 #endif
+#ifndef MPB_D52_C40
+#define MPB_D52_C40 8  // block size of the 2048-bit (D = 40) instance (tuning: 4)
+#endif
 
 namespace mpb {
 
@@ -216,7 +219,11 @@ bool launch_modexp_d52(const uint32_t* N, const uint32_t* NP, const uint32_t* R2
     };
     switch (d52_digits(bits)) {
         case 20: return go(std::integral_constant<int, 4>{}, std::integral_constant<int, 5>{});
+#if MPB_D52_C40 == 4
+        case 40: return go(std::integral_constant<int, 4>{}, std::integral_constant<int, 10>{});
+#else
         case 40: return go(std::integral_constant<int, 8>{}, std::integral_constant<int, 5>{});
+#endif
         case 64: return go(std::integral_constant<int, 8>{}, std::integral_constant<int, 8>{});
         case 80: return go(std::integral_constant<int, 8>{}, std::integral_constant<int, 10>{});
         default: return false;

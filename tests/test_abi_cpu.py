@@ -58,6 +58,9 @@ def test_host_only_helpers(lib):
     # radix-2^52 path (algo 4): D = 40 digits at 2048 bits as doubles, 2^w + 8 numbers per operand
     assert lib.mont_batch_modexp_ct_workspace(10, 2048, 5, 4) == 32 * 20 * 16 * (32 + 8)
     assert lib.mont_batch_modexp_ct_workspace(10, 700, 5, 4) == 0  # no radix-2^52 instance
+    # hybrid (algo 5): the 32-bit tiled workspace and the radix-2^52 one, side by side
+    assert lib.mont_batch_modexp_ct_workspace(10, 2048, 5, 5) == 32 * 64 * (32 + 7) * 4 + 32 * 20 * 16 * (32 + 8) + 256
+    assert lib.mont_batch_modexp_ct_workspace(10, 4096, 5, 5) == 0
     lib.mont_batch_setup_workspace.restype = ctypes.c_size_t
     lib.mont_batch_setup_workspace.argtypes = [ctypes.c_size_t, ctypes.c_int]
     assert lib.mont_batch_setup_workspace(10, 2048) == 10 * 6 * 64 * 4
@@ -118,7 +121,9 @@ def test_host_side_argument_checks(lib):
         == EUNSUPPORTED
     assert lib.mont_batch_modexp_ct(None, None, None, None, None, None, 4, 700, 5, 1, 4, None, 0, None) \
         == EUNSUPPORTED
-    assert lib.mont_batch_modexp_ct(None, None, None, None, None, None, 4, 2048, 5, 1, 5, None, 0, None) == EINVAL
+    assert lib.mont_batch_modexp_ct(None, None, None, None, None, None, 4, 2048, 5, 1, 6, None, 0, None) == EINVAL
+    assert lib.mont_batch_modexp_ct(None, None, None, None, None, None, 4, 4096, 5, 1, 5, None, 0, None) \
+        == EUNSUPPORTED  # the hybrid serves 2048-bit operands only
     lib.mp_batch_mul.argtypes = [vp, vp, vp, sz, i, i, vp, sz, vp]
     assert lib.mp_batch_mul(None, None, None, 4, 2048, 4, None, 0, None) == EUNSUPPORTED
     # CRT-RSA runs 2 * count half-size operands in one exponentiation: at most 2^26 per call
