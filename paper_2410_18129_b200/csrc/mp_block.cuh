@@ -333,4 +333,90 @@ MPB_DEVI void acc_hi(uint32_t (&W)[2 * C + 1], const uint32_t (&x)[C], const uin
     w_add<0, C + 1, 1>(W, O);
 }
 
+// ------------------------------------------------ register-level Karatsuba block
+// W[0..2C] += TW * x*y (TW = 1 or 2: the squaring's off-diagonal blocks count twice) by ONE level
+// of subtractive Karatsuba on the halves (H = C/2 limbs, X = 2^(32H); SURVEY 8(f) f1
+// with reading A4):  D0 = x0 y0, D2 = x1 y1, Dm = |x0 - x1| |y0 - y1|, s = sign(x0-x1) sign(y0-y1),
+//   x*y = D0 + (D0 + D2 - s Dm) X + D2 X^2
+// 3 H x H block products (3C^2/4 fused products instead of C^2) with shorter carry chains; the
+// sign only builds masks.  Measured on register operands (tools/microbench_kara16.cu, C = 16):
+// 28.8 vs 22.9 schoolbook-equivalent products per clock per SM at 12 warps, bit-identical.
+template <int H>
+MPB_DEVI void kara_half_product(const uint32_t (&a)[H], const uint32_t (&b)[H], uint32_t (&P)[2 * H]) {
+    uint32_t E[2 * H], O[2 * H];
+    bp_mul<H>(a, b, E, O);
+    fold_odd<H>(E, O);
+#pragma unroll
+    for (int i = 0; i < 2 * H; i++) P[i] = E[i];
+}
+template <int H>
+MPB_DEVI uint32_t kara_absdiff(const uint32_t* u, const uint32_t* v, uint32_t (&d)[H]) {
+#pragma unroll
+    for (int i = 0; i < H; i++) d[i] = u[i];
+    sub_first(d[0], v[0]);
+#pragma unroll
+    for (int i = 1; i < H; i++) sub_next(d[i], v[i]);
+    const uint32_t b = bc_save();
+    const uint32_t m = 0u - b;
+#pragma unroll
+    for (int i = 0; i < H; i++) d[i] ^= m;
+    add_first(d[0], b);
+#pragma unroll
+    for (int i = 1; i < H; i++) add_next(d[i], 0u);
+    return b;
+}
+template <int C, int TW>
+MPB_DEVI void acc_kara(uint32_t (&W)[2 * C + 1], const uint32_t (&x)[C], const uint32_t (&y)[C]) {
+    static_assert(C % 4 == 0, "halves must be even blocks");
+    constexpr int H = C / 2;
+    uint32_t dx[H], dy[H];
+    const uint32_t sx = kara_absdiff<H>(x, x + H, dx), sy = kara_absdiff<H>(y, y + H, dy);
+    uint32_t D[2 * C];  // D0 | D2 (= D0 + D2 X^2, 2C words)
+    {
+        uint32_t x0[H], y0[H], x1[H], y1[H], P[2 * H];
+#pragma unroll
+        for (int i = 0; i < H; i++) { x0[i] = x[i]; y0[i] = y[i]; x1[i] = x[H + i]; y1[i] = y[H + i]; }
+        kara_half_product<H>(x0, y0, P);
+#pragma unroll
+        for (int i = 0; i < 2 * H; i++) D[i] = P[i];
+        kara_half_product<H>(x1, y1, P);
+#pragma unroll
+        for (int i = 0; i < 2 * H; i++) D[2 * H + i] = P[i];
+    }
+    // mid = D0 + D2 - s Dm  (C + 1 words, >= 0: it is x0 y1 + x1 y0)
+    uint32_t mid[C + 1];
+#pragma unroll
+    for (int i = 0; i < C; i++) mid[i] = D[i];
+    mid[C] = 0;
+    add_first(mid[0], D[C]);
+#pragma unroll
+    for (int i = 1; i < C; i++) add_next(mid[i], D[C + i]);
+    absorb(mid[C]);
+#pragma unroll
+    for (int t = 0; t < TW; t++) {  // W += D0 + D2 X^2
+        add_first(W[0], D[0]);
+#pragma unroll
+        for (int i = 1; i < 2 * C; i++) add_next(W[i], D[i]);
+        absorb(W[2 * C]);
+    }
+    {
+        uint32_t P[2 * H];
+        kara_half_product<H>(dx, dy, P);
+        const uint32_t m = 0u - ((sx ^ sy ^ 1u) & 1u);  // all ones: subtract Dm (the signs agree)
+        cc_restore(m & 1u);                               // two's complement: + ~Dm + 1
+#pragma unroll
+        for (int i = 0; i < 2 * H; i++) add_next(mid[i], P[i] ^ m);
+        add_end(mid[C], m);
+    }
+#pragma unroll
+    for (int t = 0; t < TW; t++) {  // W += mid X  (words H .. H + C, carry to the top)
+        add_first(W[H], mid[0]);
+#pragma unroll
+        for (int i = 1; i <= C; i++) add_next(W[H + i], mid[i]);
+#pragma unroll
+        for (int i = H + C + 1; i < 2 * C; i++) add_next(W[i], 0u);
+        absorb(W[2 * C]);
+    }
+}
+
 }  // namespace mpb

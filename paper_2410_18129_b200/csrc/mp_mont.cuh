@@ -244,6 +244,15 @@ MPB_DEVI void final_select(int NB, const AR& T, const AR& OUT, uint32_t ctop, ui
 //                    FULL: alg:8MontRed lines 2-3, C = (T + q*N)/R.
 //                    Then D = C - N and a masked select give the canonical result in OUT.
 enum { PH_MUL = 0, PH_SQR = 1, PH_Q = 2, PH_HI = 3 };
+// Full (non-diagonal, non-truncated) block products by one level of register Karatsuba
+// (acc_kara) instead of the C x C schoolbook block: MPB_KARA_BLOCK = 1 (C = 16), 0 (never).
+#ifndef MPB_KARA_BLOCK
+#define MPB_KARA_BLOCK 1
+#endif
+template <int C>
+__host__ __device__ constexpr bool kara_blocks() {
+    return MPB_KARA_BLOCK && C == 16;
+}
 enum { OP_MUL = 0, OP_MUL2 = 1, OP_SQR = 2, OP_LO = 3, OP_HI = 4 };
 
 // TMA: the operand blocks of a pair are loaded per WARP as 2-D tiles (C/4 chunk rows x 32 operands
@@ -405,6 +414,9 @@ MPB_DEVI void engine(int ph, int NB, const AR& AX, const AR& AY, const AR& DST, 
             acc_lo<C>(W, x, y);
         } else if (hi_col) {
             acc_hi<C>(W, x, y);
+        } else if (kara_blocks<C>()) {  // register-level Karatsuba block (mp_block.cuh acc_kara)
+            if (sqr) acc_kara<C, 2>(W, x, y);  // s < t: the product counts twice
+            else acc_kara<C, 1>(W, x, y);
         } else {
             uint32_t E[2 * C], O[2 * C];
             bp_mul<C>(x, y, E, O);
