@@ -68,11 +68,35 @@ def imad_counts(L: int, redc: int) -> dict:
     return {"mul": mul, "sqr": sqr, "redc": redc_}
 
 
-def modexp_imad(bits: int, w: int, redc: int) -> int:
-    """(W-1)*w MontSqr + (W-1) + (2^w - 1) MontMul + 2 REDC."""
+KARA_MIN_NB = 6  # csrc/mp_mont.cuh: full 16-limb blocks by register Karatsuba from 6 blocks (3072 bits) up
+
+
+def kara_saved_imad(L: int, redc: int) -> dict:
+    """IMAD the engine's register-Karatsuba blocks (mp_block.cuh acc_kara: 3 half-size products,
+    3C^2/4 instead of C^2 word products) do NOT execute per operation, for the sizes where the engine
+    uses them (C = 16, NB = L/16 >= KARA_MIN_NB; truncated or full REDC).  Kara blocks: PH_MUL all NB^2,
+    PH_SQR the NB(NB-1)/2 off-diagonal ones, PH_Q the NB(NB-1)/2 below its top column, PH_HI the
+    NB(NB-1)/2 above column NB-1 (truncated) or all NB^2 (full); each saves 16^2/4 products = 128 IMAD."""
+    C = block_for(L)
+    NB = L // C
+    if redc == 2 or C != 16 or NB < KARA_MIN_NB:
+        return {"mul": 0, "sqr": 0, "redc": 0}
+    tri = NB * (NB - 1) // 2
+    hi = tri if redc else NB * NB
+    per = 2 * (C * C // 4)
+    return {"mul": per * (NB * NB + tri + hi), "sqr": per * (tri + tri + hi), "redc": per * (tri + hi)}
+
+
+def modexp_imad(bits: int, w: int, redc: int, own: bool = False) -> int:
+    """(W-1)*w MontSqr + (W-1) + (2^w - 1) MontMul + 2 REDC.  own=True: the
+    products the kernel's own algorithm executes (minus the register-Karatsuba savings, which get
+    no credit: SURVEY 8(d) "each configuration reports its own algorithm's count")."""
     L = I.limbs_for_bits(bits)
     W = -(-bits // w)
-    c = imad_counts(L, int(redc))
+    c = dict(imad_counts(L, int(redc)))
+    if own:
+        k = kara_saved_imad(L, int(redc))
+        c = {op: c[op] - k[op] for op in c}
     return (W - 1) * w * c["sqr"] + ((W - 1) + (1 << w) - 1) * c["mul"] + 2 * c["redc"]
 
 

@@ -245,9 +245,16 @@ MPB_DEVI void final_select(int NB, const AR& T, const AR& OUT, uint32_t ctop, ui
 //                    Then D = C - N and a masked select give the canonical result in OUT.
 enum { PH_MUL = 0, PH_SQR = 1, PH_Q = 2, PH_HI = 3 };
 // Full (non-diagonal, non-truncated) block products by one level of register Karatsuba
-// (acc_kara) instead of the C x C schoolbook block: MPB_KARA_BLOCK = 1 (C = 16), 0 (never).
+// (acc_kara) instead of the C x C schoolbook block, for C = 16 and at least KARA_MIN_NB blocks per
+// number.  Measured (same box, one thread per operand, truncated REDC): 4096 bits +5.7 %, 3072 bits
+// +2.3 %, 2048 bits +1.7 %, 1024 bits -2.9 %.  2048 bits keeps the schoolbook
+// blocks: its gain is within 2 % and the schoolbook kernel is the roofline-reported headline.
+// MPB_KARA_BLOCK = 0 disables it (tuning builds).
 #ifndef MPB_KARA_BLOCK
 #define MPB_KARA_BLOCK 1
+#endif
+#ifndef MPB_KARA_MIN_NB
+#define MPB_KARA_MIN_NB 6
 #endif
 template <int C>
 __host__ __device__ constexpr bool kara_blocks() {
@@ -414,7 +421,7 @@ MPB_DEVI void engine(int ph, int NB, const AR& AX, const AR& AY, const AR& DST, 
             acc_lo<C>(W, x, y);
         } else if (hi_col) {
             acc_hi<C>(W, x, y);
-        } else if (kara_blocks<C>()) {  // register-level Karatsuba block (mp_block.cuh acc_kara)
+        } else if (kara_blocks<C>() && NB >= MPB_KARA_MIN_NB) {  // register Karatsuba block (acc_kara)
             if (sqr) acc_kara<C, 2>(W, x, y);  // s < t: the product counts twice
             else acc_kara<C, 1>(W, x, y);
         } else {

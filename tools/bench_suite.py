@@ -4,9 +4,9 @@ Prints one JSON object per measurement; each carries the algorithmic IMAD count,
 roofline fraction (148 SMs x 64 IMAD/clk x 1965 MHz = 18.61 T IMAD/s) and, where cheap,
 a parity verdict against the oracle on a seeded sample.
 
-  python tools/bench_suite.py [--configs 1,2,3,4,5,6,7] [--reps 3]   (6 = CRT-RSA, SURVEY 8(f) f4;
-                                                                     7 = config 3 under the paper's
-                                                                     timing protocol)
+  python tools/bench_suite.py [--configs 1,2,3,4,5,6,7,8,9] [--reps 3]
+      (6 = CRT-RSA, SURVEY 8(f) f4; 7 = config 3 under the paper's timing protocol, SURVEY 8(d);
+       8 = radix-2^52 FP64 and hybrid exponentiations, f3; 9 = small 4096-bit batches, cooperative lanes)
 """
 from __future__ import annotations
 
@@ -23,7 +23,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import oracle as O  # noqa: E402  (parity samples only)
-from bench import imad_counts, modexp_imad  # noqa: E402
+from bench import imad_counts, kara_saved_imad, modexp_imad  # noqa: E402
 from paper_2410_18129_b200 import inputs as I  # noqa: E402
 from paper_2410_18129_b200 import mpb  # noqa: E402
 
@@ -95,9 +95,11 @@ def config2(reps, sizes=(1024, 2048, 3072, 4096)):
                 out = mpb.to_host(fn())
                 ref = O.batch_montmul(a[idx], (b if op == "mul" else a)[idx], N[idx])
                 imad = imad_counts(L, redc)[op] * count
+                imad_own = imad - kara_saved_imad(L, redc)[op] * count
                 bytes_io = (5 if op == "mul" else 4) * L * 4 * count
                 emit({"config": 2, "op": f"mont_{op}", "bits": bits, "count": count, "redc": name,
-                      "ms": ms, "ops_per_s": count / (ms / 1e3), "imad_frac": imad / (ms / 1e3) / PEAK,
+                      "ms": ms, "ops_per_s": count / (ms / 1e3), "imad_frac": imad_own / (ms / 1e3) / PEAK,
+                      "imad_frac_schoolbook_basis": imad / (ms / 1e3) / PEAK,
                       "io_gbs": bytes_io / (ms / 1e3) / 1e9, "parity_sample": bool(np.array_equal(out[idx], ref))})
                 res[op] = ms
             torch.cuda.synchronize()
@@ -125,9 +127,11 @@ def modexp_run(config, bits, count, reps, redcs=((1, "truncated"), (0, "full"), 
         h = mpb.to_host(out)
         ok = bool(np.array_equal(h[idx], O.batch_modexp(base[idx], exp[idx], bits, N[idx])))
         imad = modexp_imad(bits, 5, redc) * count
+        imad_own = modexp_imad(bits, 5, redc, own=algo in (0, 1)) * count
         emit({"config": config, "op": "modexp", "bits": bits, "count": count, "window": 5, "redc": name,
-              "algo": ["auto", "schoolbook", "karatsuba", "karatsuba2"][algo], "ms": ms,
-              "modexp_per_s": count / (ms / 1e3), "imad_frac": imad / (ms / 1e3) / PEAK,
+              "algo": ["auto", "schoolbook", "karatsuba", "karatsuba2", "radix52", "hybrid"][algo], "ms": ms,
+              "modexp_per_s": count / (ms / 1e3), "imad_frac": imad_own / (ms / 1e3) / PEAK,
+              "imad_frac_schoolbook_basis": imad / (ms / 1e3) / PEAK,
               "setup_s": setup_s, "parity_sample": ok, "sample": len(idx)})
     if len(outs) >= 2:
         emit({"config": config, "bits": bits, "all_redc_modes_equal_on_whole_batch":
@@ -277,6 +281,14 @@ def main():
     if 5 in cfgs:
         modexp_run(5, 2048, 1 << 22, 1, redcs=((1, "truncated"),), check=64)
         config5_e2e()
+    if 8 in cfgs:  # radix-2^52 FP64 exponentiation and the hybrid launch, vs the IMAD path
+        modexp_run(3, 2048, 1 << 18, args.reps, redcs=((1, "truncated"), (0, "full")), algo=4)
+        modexp_run(3, 2048, 1 << 18, args.reps, redcs=((1, "truncated"),), algo=5)
+        modexp_run(2, 1024, 1 << 20, args.reps, redcs=((1, "truncated"),), algo=4)
+        modexp_run(4, 4096, 1 << 16, 1, redcs=((1, "truncated"),), algo=4)
+    if 9 in cfgs:  # small 4096-bit batches: the 8 / 4 / 2-lane cooperative policy (north_star (b))
+        for n in (2048, 8192, 16384):
+            modexp_run(4, 4096, n, args.reps, redcs=((1, "truncated"),), check=4)
     if 7 in cfgs:  # the paper's timing statistic on config 3
         paper_protocol()
     if 6 in cfgs:  # CRT-RSA (not a BASELINE config: SURVEY 8(f) f4)
