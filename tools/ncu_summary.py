@@ -12,7 +12,7 @@ rows = list(csv.reader(io.StringIO(raw)))
 hdr, units, vals = rows[0], rows[1], rows[2]
 pat = (r"^gpu__time_duration.sum$|^launch__registers_per_thread$|^launch__grid_size$|^launch__block_size$|"
        r"^sm__warps_active.avg.pct_of_peak_sustained_active$|^sm__issue_active.avg.pct_of_peak_sustained_active$|"
-       r"^sm__pipe_(fma|alu|fmaheavy)_cycles_active.avg.pct_of_peak_sustained_active$|"
+       r"^sm__pipe_(fma|alu|fmaheavy|fp64)_cycles_active.avg.pct_of_peak_sustained_(active|elapsed)$|^smsp__issue_active.avg.pct_of_peak_sustained_active$|"
        r"^dram__bytes_(read|write).sum$|^dram__throughput.avg.pct_of_peak_sustained_elapsed$|"
        r"^l1tex__t_sector_hit_rate.pct$|^lts__t_sector_hit_rate.pct$|^smsp__inst_executed.sum$|"
        r"^smsp__sass_inst_executed_op_local_(ld|st).sum$|^sm__cycles_elapsed.avg.per_second$|"
