@@ -16,13 +16,14 @@ ap.add_argument("--window", type=int, default=5)
 ap.add_argument("--redc", type=int, default=1)
 ap.add_argument("--op", default="modexp", choices=["modexp", "montmul", "montsqr"])
 ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--algo", type=int, default=0)
 a = ap.parse_args()
 N, base, exp = I.modexp_inputs(config=3, count=a.count, bits=a.bits)
 dN, dB, dE = (mpb.to_device(x) for x in (N, base, exp))
 Np, R2 = mpb.mont_batch_setup(dN, a.bits)
 for _ in range(a.reps):
     if a.op == "modexp":
-        out = mpb.mont_batch_modexp_ct(dN, Np, R2, dB, dE, a.bits, a.window, a.redc)
+        out = mpb.mont_batch_modexp_ct(dN, Np, R2, dB, dE, a.bits, a.window, a.redc, algo=a.algo)
     elif a.op == "montmul":
         out = mpb.mont_batch_mul(dB, dE, dN, Np, a.bits, a.redc)
     else:
