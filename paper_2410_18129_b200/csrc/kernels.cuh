@@ -357,8 +357,8 @@ MPB_DEVI void modexp_body(const uint32_t* N, const uint32_t* NP, const uint32_t*
 }
 
 // One thread per operand: operands k_ofs .. k_ofs + n_run - 1 of a batch of `count`.
-template <int C, int RM, int NBT, int KLEV>
-__global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_modexp(
+template <int C, int RM, int NBT, int KLEV, int MINB = min_blocks<C>()>
+__global__ void __launch_bounds__(kThreads, MINB) k_modexp(
     const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP, const uint32_t* __restrict__ R2,
     const uint32_t* __restrict__ base, const uint32_t* __restrict__ exp, uint32_t* __restrict__ out, size_t count,
     size_t k_ofs, size_t n_run, int nb_rt, int bits, int w, uint32_t* ws) {
@@ -721,6 +721,24 @@ void Launch<C>::modexp(const uint32_t* N, const uint32_t* NP, const uint32_t* R2
             if constexpr (NBT == 0 || NBT == 8 || NBT == 11) {
                 if (levels >= 2) return go(std::integral_constant<int, 2>{});
                 if (levels == 1) return go(std::integral_constant<int, 1>{});
+            }
+            if constexpr (C == 16 && NBT == 8) {
+                // 4096 bits: a batch that needs two waves at 3 CTAs per SM but fits ONE wave at 4
+                // (128 registers, a few spills) runs the 4-CTA instance -- config 4 (2^16 operands,
+                // 1.15 waves at 3 CTAs): 46.1 K vs 44.3 K/s measured; many-wave batches keep 3 CTAs
+                // (the 4-CTA instance is slower per operand).  DESIGN.md 5.3b.
+                int dev = 0, sms = 148;
+                if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+                const size_t w3 = (size_t)sms * kThreads * min_blocks<C>(), w4 = (size_t)sms * kThreads * 4;
+                if (n > w3 && n <= w4 && min_blocks<C>() < 4 && redc != 2) {
+                    if (redc == 1)
+                        k_modexp<C, 1, NBT, 0, 4><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, k0, n, nb,
+                                                                          bits, window, ws);
+                    else
+                        k_modexp<C, 0, NBT, 0, 4><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, k0, n, nb,
+                                                                          bits, window, ws);
+                    return;
+                }
             }
             go(std::integral_constant<int, 0>{});
         };
