@@ -97,6 +97,16 @@ int check_launch() {
 
 unsigned grid_for(size_t n) { return (unsigned)((n + kThreads - 1) / kThreads); }
 
+// MPB_REG=0 routes 1024-bit CIOS exponentiations to the block engine instead of the register-resident
+// kernel (tests and A/B only)
+int reg_policy() {
+    static int v = [] {
+        const char* e = getenv("MPB_REG");
+        return e ? atoi(e) : 1;
+    }();
+    return v;
+}
+
 // The library's own stream-ordered memory pool for the current device (mpb_modexp_host), created
 // once per device with an unlimited release threshold so repeated calls reuse their allocation;
 // the device's default pool (and every other cudaMallocAsync user in the process) is untouched.
@@ -324,6 +334,11 @@ int mont_batch_modexp_ct(const uint32_t* N, const uint32_t* NP, const uint32_t* 
         return fail(MPB_EINVAL, "output aliases an input");
     if (ws_bytes < mont_batch_modexp_ct_workspace(count, bits, window, algo))
         return fail(MPB_EINVAL, "workspace too small");
+    if (redc == MPB_REDC_CIOS && L == 32 && algo <= MPB_ALGO_SCHOOLBOOK && reg_policy() != 0) {
+        // 1024 bits, CIOS: the register-resident exponentiation (inst_R32.cu)
+        mpb::launch_modexp_reg(N, NP, R2, base, exp, out, count, bits, window, (uint32_t*)ws, (cudaStream_t)stream);
+        return check_launch();
+    }
     if (algo == MPB_ALGO_HYBRID) {
         mpb::launch_modexp_hybrid(N, NP, R2, base, exp, out, count, bits, window, redc == MPB_REDC_TRUNCATED,
                                   (uint32_t*)ws, (cudaStream_t)stream);

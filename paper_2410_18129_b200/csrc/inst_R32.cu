@@ -1,0 +1,146 @@
+// inst_R32.cu -- the register-resident CIOS exponentiation for 1024-bit operands (mp_reg.cuh).
+//
+// mont_batch_modexp_ct with redc = MPB_REDC_CIOS and L = 32 limbs (897..1024 bits) runs this kernel:
+// alg:8FWExp on alg:8BlockMontRed MontMuls whose accumulator, multiplicand
+// and modulus live in registers (mp_reg.cuh); the a operand of each MontMul is streamed from a
+// per-thread shared-memory slot (one LDS per row), the 2^w-entry table lives in the warp-tiled
+// workspace and is read by the masked full scan.  One flat public schedule with a single
+// MontMul call site, as k_modexp: the kernel is one straight-line MontMul plus control.
+#include "kernels.cuh"
+#include "mp_reg.cuh"
+
+#ifndef MPB_REG_MINB
+#define MPB_REG_MINB 3
+#endif
+
+namespace mpb {
+
+template <int L>
+__global__ void __launch_bounds__(kThreads, MPB_REG_MINB) k_modexp_reg(
+    const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP, const uint32_t* __restrict__ R2,
+    const uint32_t* __restrict__ base, const uint32_t* __restrict__ exp, uint32_t* __restrict__ out, size_t count,
+    int bits, int w, uint32_t* ws) {
+    const size_t k = tid_global();
+    if (k >= count) return;
+    constexpr int Q4 = L / 4;
+    const int nent = 1 << w;
+    extern __shared__ __align__(16) uint32_t smem_a[];  // word q of this thread at q * blockDim + tid
+    uint32_t* const sa = smem_a + threadIdx.x;
+    const ArrT G = tarr(ws, nent * Q4, k);
+    const Arr Nn = arr(N, count, k), R2n = arr(R2, count, k), Bn = arr(base, count, k), On = arr(out, count, k);
+    uint32_t n[L];
+    ldb<L>(Nn, 0, n);
+    const uint32_t n0p = word_at(NP, count, k, 0);  // n0' = N'[0] (reading A10)
+    auto aw = [&](int i) { return sa[i * kThreads]; };
+    auto a_from_regs = [&](const uint32_t (&x)[L]) {
+#pragma unroll
+        for (int q = 0; q < L; q++) sa[q * kThreads] = x[q];
+    };
+    auto a_from_mem = [&](const auto& A) {
+#pragma unroll
+        for (int q = 0; q < Q4; q++) {
+            const uint4 v = A.ld(q);
+            sa[(4 * q) * kThreads] = v.x;
+            sa[(4 * q + 1) * kThreads] = v.y;
+            sa[(4 * q + 2) * kThreads] = v.z;
+            sa[(4 * q + 3) * kThreads] = v.w;
+        }
+    };
+    const int nwin = (bits + w - 1) / w;
+    auto window = [&](int win) {
+        const int pos = win * w, wi = pos >> 5, off = pos & 31;
+        uint32_t v = word_at(exp, count, k, wi) >> off;
+        if (off + w > 32 && wi + 1 < L) v |= word_at(exp, count, k, wi + 1) << (32 - off);
+        return v & ((1u << w) - 1u);
+    };
+    // CT masked full-table scan into the a slot
+    auto select = [&](uint32_t idx) {
+        uint4 acc[Q4];
+#pragma unroll
+        for (int q = 0; q < Q4; q++) acc[q] = make_uint4(0, 0, 0, 0);
+#pragma unroll 1
+        for (int e = 0; e < nent; e++) {
+            const uint32_t x = (uint32_t)e ^ idx;
+            const uint32_t m = 0u - ((x - 1u) >> 31);  // all ones iff e == idx
+            const ArrT Ge = G.at(e * Q4);
+#pragma unroll
+            for (int q = 0; q < Q4; q++) {
+                const uint4 v = Ge.ld_stream(q);
+                acc[q].x |= v.x & m;
+                acc[q].y |= v.y & m;
+                acc[q].z |= v.z & m;
+                acc[q].w |= v.w & m;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < Q4; q++) {
+            sa[(4 * q) * kThreads] = acc[q].x;
+            sa[(4 * q + 1) * kThreads] = acc[q].y;
+            sa[(4 * q + 2) * kThreads] = acc[q].z;
+            sa[(4 * q + 3) * kThreads] = acc[q].w;
+        }
+    };
+    // Flat schedule (public): op 0 G[0] = MontMul(R2, 1) (Montgomery one), op 1 G[1] = MontMul(base, R2),
+    // op e < 2^w G[e] = MontMul(G[e-1], G[1]); then Y = G[top window]; per window w squarings, select,
+    // one multiplication; last op out = MontMul(Y, 1).
+    uint32_t y[L];
+#pragma unroll
+    for (int q = 0; q < L; q++) y[q] = 0;
+    const int per_win = w + 1;
+    const int n_ops = nent + (nwin - 1) * per_win + 1;
+#pragma unroll 1
+    for (int op = 0; op < n_ops; op++) {
+        uint32_t b[L];
+        int store_e = -1;
+        bool b_one = false, b_y = true;
+        if (op < nent) {
+            store_e = op;
+            if (op == 0) {
+                a_from_mem(R2n);
+                b_one = true;
+            } else if (op == 1) {
+                a_from_mem(Bn);
+                ldb<L>(R2n, 0, b);
+                b_y = false;
+            } else {
+                a_from_mem(G.at((op - 1) * Q4));
+                ldb<L>(G.at(Q4), 0, b);
+                b_y = false;
+            }
+        } else if (op == n_ops - 1) {
+            a_from_regs(y);
+            b_one = true;
+        } else {
+            const int r = (op - nent) % per_win, win = nwin - 2 - (op - nent) / per_win;
+            if (r < w) a_from_regs(y);  // squaring: a = b = Y
+            else select(window(win));   // multiplication by the selected entry
+        }
+        if (b_one) {
+#pragma unroll
+            for (int q = 0; q < L; q++) b[q] = q == 0 ? 1u : 0u;
+        } else if (b_y) {
+#pragma unroll
+            for (int q = 0; q < L; q++) b[q] = y[q];
+        }
+        reg::montmul<L>(aw, b, n, n0p, y);
+        if (store_e >= 0) stb<L>(G.at(store_e * Q4), 0, y);
+        if (op == nent - 1) {  // after the table: Y = G[top window]
+            select(window(nwin - 1));
+#pragma unroll
+            for (int q = 0; q < L; q++) y[q] = aw(q);
+        }
+    }
+    stb<L>(On, 0, y);
+}
+
+bool launch_modexp_reg(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
+                       const uint32_t* exp, uint32_t* out, size_t count, int bits, int window, uint32_t* ws,
+                       cudaStream_t s) {
+    if (4 * ((bits + 127) / 128) != 32) return false;
+    const unsigned g = (unsigned)((count + kThreads - 1) / kThreads);
+    k_modexp_reg<32><<<g, kThreads, (size_t)kThreads * 32 * 4, s>>>(N, NP, R2, base, exp, out, count, bits, window,
+                                                                  ws);
+    return true;
+}
+
+}  // namespace mpb

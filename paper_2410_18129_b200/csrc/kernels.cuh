@@ -589,6 +589,7 @@ void with_nb(int nb, F&& f) {
         if (nb == 11) return f(std::integral_constant<int, 11>{});
     } else if constexpr (C == 8) {
         switch (nb) {
+            case 4: return f(std::integral_constant<int, 4>{});  // 1024 bits with MPB_BLOCK=8 (tuning)
             case 8: return f(std::integral_constant<int, 8>{});
             case 16: return f(std::integral_constant<int, 16>{});
             default: break;

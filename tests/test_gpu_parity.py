@@ -337,6 +337,35 @@ def test_modexp_host_e2e(mpb):
     assert np.array_equal(out, O.batch_modexp(base, exp, bits, N))
 
 
+# ------------------------------------------ register-resident CIOS (1024 bits)
+@pytest.mark.parametrize("count,window", [(1, 5), (33, 1), (33, 6), (300, 5), (129, 4)])
+def test_modexp_cios_register_kernel(mpb, count, window):
+    """1024-bit CIOS exponentiation: the register-resident kernel (mp_reg.cuh, inst_R32.cu: rows
+    fully unrolled, accumulator / multiplicand / modulus in registers) against the oracle, ragged
+    counts, windows 1..6, plus edge operands (0^0, base 0, base N-1, all-ones exponent, N = 2^1024-1,
+    N = 2^1023+1)."""
+    bits = 1024
+    L = I.limbs_for_bits(bits)
+    N, base, exp = I.modexp_inputs(config=1, count=count, bits=bits, dataset=count + window)
+    if count >= 12:
+        N[0] = np.uint32(0xFFFFFFFF)
+        N[1] = 0
+        N[1, 0] = 1
+        N[1, L - 1] = np.uint32(1 << 31)
+        Ns = ints(N)
+        cases = [(5, 7), (Ns[1] - 1, 12), (0, 0), (0, 9), (1, (1 << bits) - 1), (Ns[5] - 1, 3), (2, Ns[6] - 1),
+                 (Ns[7] - 2, (1 << bits) - 1), (Ns[8] // 3, 1), (3, 1 << (bits - 1)), (Ns[10] - 1, 2),
+                 (Ns[11] - 1, (1 << bits) - 2)]
+        for k, (bv, ev) in enumerate(cases):
+            base[k] = I.to_limbs(bv, L)
+            exp[k] = I.to_limbs(ev, L)
+    dN = mpb.to_device(N)
+    Np, R2 = mpb.mont_batch_setup(dN, bits)
+    out = mpb.to_host(mpb.mont_batch_modexp_ct(dN, Np, R2, mpb.to_device(base), mpb.to_device(exp), bits,
+                                               window=window, redc=mpb.REDC_CIOS))
+    assert np.array_equal(out, O.batch_modexp(base, exp, bits, N))
+
+
 # ------------------------------------------------- radix-2^52 FP64 path (f3)
 BITS_D52 = [1024, 2048, 3072, 4096, 4108]
 D52_COUNTS = {1024: 40, 2048: 37, 3072: 5, 4096: 3, 4108: 3}
