@@ -57,9 +57,10 @@ def imad_counts(L: int, redc: int) -> dict:
     a lo-only product = 1; the hi-only products of column L-2 count 1 each.
     redc: 1 truncated, 0 full, 2 CIOS (alg:8BlockMontRed at digit 2^(32C): per row of C limbs,
     2CL products for a_i*B, 2CL for m_i*N and a C x C low-half product of C^2 IMAD, so
-    4L^2 + LC for a multiplication or a squaring; REDC is MontMul(X, 1))."""
+    4L^2 + LC for a multiplication or a squaring; REDC is MontMul(X, 1).  At L = 32 the
+    register-resident kernel (csrc/mp_reg.cuh) uses the paper's word digit: C = 1, 4L^2 + L)."""
     if redc == 2:
-        C = block_for(L)
+        C = 1 if L == 32 else block_for(L)  # 1024 bits: the register-resident kernel's 32-bit digit
         mul = sqr = redc_ = 4 * L * L + L * C
     elif redc:
         mul, sqr, redc_ = 4 * L * L + 2 * L - 1, 3 * L * L + 3 * L - 1, 2 * L * L + 2 * L - 1
