@@ -133,6 +133,179 @@ __global__ void __launch_bounds__(kThreads, MPB_REG_MINB) k_modexp_reg(
     stb<L>(On, 0, y);
 }
 
+// Stand-alone CIOS MontMul / MontSqr at L = 32 (mont_batch_mul / mont_batch_sqr, redc = CIOS):
+// c = a b 2^(-1024) mod N canonical, the register-resident row loop of mp_reg.cuh.
+template <int L>
+__global__ void __launch_bounds__(kThreads, MPB_REG_MINB) k_mont_mul_reg(
+    const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, const uint32_t* __restrict__ N,
+    const uint32_t* __restrict__ NP, uint32_t* __restrict__ c, size_t count) {
+    const size_t k = tid_global();
+    if (k >= count) return;
+    extern __shared__ __align__(16) uint32_t smem_a[];
+    uint32_t* const sa = smem_a + threadIdx.x;
+    const Arr A = arr(a, count, k);
+#pragma unroll
+    for (int q = 0; q < L / 4; q++) {
+        const uint4 v = A.ld(q);
+        sa[(4 * q) * kThreads] = v.x;
+        sa[(4 * q + 1) * kThreads] = v.y;
+        sa[(4 * q + 2) * kThreads] = v.z;
+        sa[(4 * q + 3) * kThreads] = v.w;
+    }
+    uint32_t bb[L], n[L], y[L];
+    ldb<L>(arr(b, count, k), 0, bb);
+    ldb<L>(arr(N, count, k), 0, n);
+    const uint32_t n0p = word_at(NP, count, k, 0);
+    reg::montmul<L>([&](int i) { return sa[i * kThreads]; }, bb, n, n0p, y);
+    stb<L>(arr(c, count, k), 0, y);
+}
+
+// Register-resident TRUNCATED exponentiation at L = 32 (mont_batch_modexp_ct, redc = truncated):
+// reg::montmul_trunc (alg:trunc_montred + Theorem 2 at word granularity) as MontSqr and MontMul
+// instances, one call site each, inside the same flat public schedule as k_modexp_reg.  Per-thread
+// shared memory (word q of thread t at q * blockDim + t): the a operand, N, N', T's high half.
+template <int L>
+__global__ void __launch_bounds__(kThreads, MPB_REG_MINB) k_modexp_rtr(
+    const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP, const uint32_t* __restrict__ R2,
+    const uint32_t* __restrict__ base, const uint32_t* __restrict__ exp, uint32_t* __restrict__ out, size_t count,
+    int bits, int w, uint32_t* ws) {
+    const size_t k = tid_global();
+    if (k >= count) return;
+    constexpr int Q4 = L / 4;
+    constexpr int SL = L * kThreads;  // words per shared-memory region
+    const int nent = 1 << w;
+    extern __shared__ __align__(16) uint32_t smem_a[];
+    uint32_t* const sa = smem_a + threadIdx.x;  // a operand
+    uint32_t* const sn = sa + SL;               // N
+    uint32_t* const snp = sa + 2 * SL;          // N'
+    uint32_t* const sth = sa + 3 * SL;          // T high half
+    const ArrT G = tarr(ws, nent * Q4, k);
+    const Arr Nn = arr(N, count, k), NPn = arr(NP, count, k), R2n = arr(R2, count, k), Bn = arr(base, count, k),
+              On = arr(out, count, k);
+    auto to_slot = [&](uint32_t* slot, const auto& A) {
+#pragma unroll
+        for (int q = 0; q < Q4; q++) {
+            const uint4 v = A.ld(q);
+            slot[(4 * q) * kThreads] = v.x;
+            slot[(4 * q + 1) * kThreads] = v.y;
+            slot[(4 * q + 2) * kThreads] = v.z;
+            slot[(4 * q + 3) * kThreads] = v.w;
+        }
+    };
+    to_slot(sn, Nn);
+    to_slot(snp, NPn);
+    auto aw = [&](int i) { return sa[i * kThreads]; };
+    auto nw = [&](int j) { return sn[j * kThreads]; };
+    auto npw = [&](int j) { return snp[j * kThreads]; };
+    auto thw = [&](int i, uint32_t v) { sth[i * kThreads] = v; };
+    auto thr = [&](int i) { return sth[i * kThreads]; };
+    const int nwin = (bits + w - 1) / w;
+    auto window = [&](int win) {
+        const int pos = win * w, wi = pos >> 5, off = pos & 31;
+        uint32_t v = word_at(exp, count, k, wi) >> off;
+        if (off + w > 32 && wi + 1 < L) v |= word_at(exp, count, k, wi + 1) << (32 - off);
+        return v & ((1u << w) - 1u);
+    };
+    auto select = [&](uint32_t idx) {  // CT masked full-table scan into the a slot
+        uint4 acc[Q4];
+#pragma unroll
+        for (int q = 0; q < Q4; q++) acc[q] = make_uint4(0, 0, 0, 0);
+#pragma unroll 1
+        for (int e = 0; e < nent; e++) {
+            const uint32_t x = (uint32_t)e ^ idx;
+            const uint32_t m = 0u - ((x - 1u) >> 31);
+            const ArrT Ge = G.at(e * Q4);
+#pragma unroll
+            for (int q = 0; q < Q4; q++) {
+                const uint4 v = Ge.ld_stream(q);
+                acc[q].x |= v.x & m;
+                acc[q].y |= v.y & m;
+                acc[q].z |= v.z & m;
+                acc[q].w |= v.w & m;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < Q4; q++) {
+            sa[(4 * q) * kThreads] = acc[q].x;
+            sa[(4 * q + 1) * kThreads] = acc[q].y;
+            sa[(4 * q + 2) * kThreads] = acc[q].z;
+            sa[(4 * q + 3) * kThreads] = acc[q].w;
+        }
+    };
+    uint32_t y[L];
+#pragma unroll
+    for (int q = 0; q < L; q++) y[q] = 0;
+    const int per_win = w + 1;
+    const int n_ops = nent + (nwin - 1) * per_win + 1;
+#pragma unroll 1
+    for (int op = 0; op < n_ops; op++) {
+        uint32_t b[L];
+        int store_e = -1;
+        bool b_one = false, b_y = true, sqr = false;
+        if (op < nent) {
+            store_e = op;
+            if (op == 0) {
+                to_slot(sa, R2n);
+                b_one = true;
+            } else if (op == 1) {
+                to_slot(sa, Bn);
+                ldb<L>(R2n, 0, b);
+                b_y = false;
+            } else {
+                to_slot(sa, G.at((op - 1) * Q4));
+                ldb<L>(G.at(Q4), 0, b);
+                b_y = false;
+            }
+        } else if (op == n_ops - 1) {
+#pragma unroll
+            for (int q = 0; q < L; q++) sa[q * kThreads] = y[q];
+            b_one = true;
+        } else {
+            const int r = (op - nent) % per_win, win = nwin - 2 - (op - nent) / per_win;
+            if (r < w) sqr = true;
+            else select(window(win));
+        }
+        if (b_one) {
+#pragma unroll
+            for (int q = 0; q < L; q++) b[q] = q == 0 ? 1u : 0u;
+        } else if (b_y) {
+#pragma unroll
+            for (int q = 0; q < L; q++) b[q] = y[q];
+        }
+        reg::montmul_trunc<L>(sqr, aw, b, npw, nw, thw, thr, y);
+        if (store_e >= 0) stb<L>(G.at(store_e * Q4), 0, y);
+        if (op == nent - 1) {
+            select(window(nwin - 1));
+#pragma unroll
+            for (int q = 0; q < L; q++) y[q] = aw(q);
+        }
+    }
+    stb<L>(On, 0, y);
+}
+
+bool launch_modexp_rtr(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
+                       const uint32_t* exp, uint32_t* out, size_t count, int bits, int window, uint32_t* ws,
+                       cudaStream_t s) {
+    if (4 * ((bits + 127) / 128) != 32) return false;
+    const unsigned g = (unsigned)((count + kThreads - 1) / kThreads);
+    const size_t sm = (size_t)kThreads * 32 * 4 * 4;  // a, N, N', T_high
+    static bool attr = [] {
+        return cudaFuncSetAttribute(k_modexp_rtr<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024) ==
+               cudaSuccess;
+    }();
+    (void)attr;
+    k_modexp_rtr<32><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, bits, window, ws);
+    return true;
+}
+
+bool launch_mont_mul_reg(const uint32_t* a, const uint32_t* b, const uint32_t* N, const uint32_t* NP, uint32_t* c,
+                         size_t count, int bits, cudaStream_t s) {
+    if (4 * ((bits + 127) / 128) != 32) return false;
+    const unsigned g = (unsigned)((count + kThreads - 1) / kThreads);
+    k_mont_mul_reg<32><<<g, kThreads, (size_t)kThreads * 32 * 4, s>>>(a, b, N, NP, c, count);
+    return true;
+}
+
 bool launch_modexp_reg(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
                        const uint32_t* exp, uint32_t* out, size_t count, int bits, int window, uint32_t* ws,
                        cudaStream_t s) {

@@ -60,6 +60,13 @@ bool launch_modexp_reg(const uint32_t* N, const uint32_t* NP, const uint32_t* R2
                        const uint32_t* exp, uint32_t* out, size_t count, int bits, int window, uint32_t* ws,
                        cudaStream_t s);
 
+// register-resident TRUNCATED exponentiation for L = 32 limbs (inst_R32.cu)
+bool launch_modexp_rtr(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
+                       const uint32_t* exp, uint32_t* out, size_t count, int bits, int window, uint32_t* ws,
+                       cudaStream_t s);
+bool launch_mont_mul_reg(const uint32_t* a, const uint32_t* b, const uint32_t* N, const uint32_t* NP, uint32_t* c,
+                         size_t count, int bits, cudaStream_t s);
+
 // scratch blocks of the Karatsuba product (mirror of mp_kara.cuh kara_scratch_blocks)
 inline int kara_scratch_blocks_host(int nb, int level) {
     return level <= 0 || nb < 2 ? 0 : 4 * ((nb + 1) / 2) + kara_scratch_blocks_host((nb + 1) / 2, level - 1);

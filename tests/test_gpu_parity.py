@@ -366,6 +366,51 @@ def test_modexp_cios_register_kernel(mpb, count, window):
     assert np.array_equal(out, O.batch_modexp(base, exp, bits, N))
 
 
+_RTR_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+from paper_2410_18129_b200 import inputs as I, mpb
+bits = 1024
+L = I.limbs_for_bits(bits)
+for count, w, ds in ((37, 5, 1), (300, 4, 2), (9, 1, 3), (33, 6, 4)):
+    N, base, exp = I.modexp_inputs(config=1, count=count, bits=bits, dataset=ds)
+    if count >= 12:
+        N[0] = np.uint32(0xFFFFFFFF)
+        N[1] = 0; N[1, 0] = 1; N[1, L - 1] = np.uint32(1 << 31)
+        base[2] = 0; exp[2] = 0
+        base[3] = 0
+        base[4] = 0; base[4, 0] = 1
+        exp[5] = np.uint32(0xFFFFFFFF)
+    dN = mpb.to_device(N)
+    Np, R2 = mpb.mont_batch_setup(dN, bits)
+    o = mpb.to_host(mpb.mont_batch_modexp_ct(dN, Np, R2, mpb.to_device(base), mpb.to_device(exp), bits, window=w,
+                                             redc=mpb.REDC_TRUNCATED))
+    print(count, w, ds, N.tobytes().hex(), base.tobytes().hex(), exp.tobytes().hex(), o.tobytes().hex())
+"""
+
+
+def test_modexp_truncated_register_kernel(mpb):
+    """The register-resident truncated exponentiation at 1024 bits (mp_reg.cuh montmul_trunc:
+    word-level alg:trunc_montred with Theorem 2's correction), forced with MPB_REG=2 in a
+    subprocess, against the oracle: ragged counts, windows 1..6, edge operands and moduli."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, "-c", _RTR_SCRIPT % root], env=dict(os.environ, MPB_REG="2"),
+                         capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [l for l in res.stdout.splitlines() if l.strip()]
+    assert len(lines) == 4
+    L = 32
+    for line in lines:
+        count, w, ds, hn, hb, he, ho = line.split()
+        count = int(count)
+        N, base, exp, got = (np.frombuffer(bytes.fromhex(h), dtype=np.uint32).reshape(count, L) for h in (hn, hb, he, ho))
+        assert np.array_equal(got, O.batch_modexp(base, exp, 1024, N)), (count, w)
+
+
 # ------------------------------------------------- radix-2^52 FP64 path (f3)
 BITS_D52 = [1024, 2048, 3072, 4096, 4108]
 D52_COUNTS = {1024: 40, 2048: 37, 3072: 5, 4096: 3, 4108: 3}
