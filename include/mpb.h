@@ -55,7 +55,8 @@ enum { MPB_ALGO_AUTO = 0, MPB_ALGO_SCHOOLBOOK = 1, MPB_ALGO_KARATSUBA = 2, MPB_A
 /* RADIX52 (mont_batch_modexp_ct only): the exponentiation runs internally on 52-bit limbs held in
  * doubles, every word product split exactly into its low and high 52-bit halves by two FP64 fused
  * multiply-adds (the paper's own radix and madd52lo/hi) and summed without carries;
- * Montgomery reduction modulo 2^(52D) with truncated or full REDC (not CIOS).  Same inputs (the
+ * Montgomery reduction modulo 2^(52D) with truncated or full REDC, or -- at 1024 bits only -- CIOS
+ * (a register-resident kernel, the paper's word-level alg:8BlockMontRed in its own radix).  Same inputs (the
  * 32-bit N', R^2 mod N: the 52-bit constants are derived in the kernel), same canonical result.
  * Sizes: bits with a D in {20, 40, 64, 80} such that 52D >= bits + 2 and 0 <= 130D - 64L <= bits - 2
  * (1024, 2048, 3072, 4096 and 4108 bits among them); other sizes MPB_EUNSUPPORTED.

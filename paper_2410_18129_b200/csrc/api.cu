@@ -302,7 +302,10 @@ int mont_batch_redc(const uint32_t* T, const uint32_t* N, const uint32_t* NP, ui
 size_t mont_batch_modexp_ct_workspace(size_t count, int bits, int window, int algo) {
     const int L = mpb_limbs(bits);
     if (L <= 0 || window < 1 || window > 6) return 0;
-    if (algo == MPB_ALGO_RADIX52) return mpb::d52_workspace_bytes(count, bits, window);
+    if (algo == MPB_ALGO_RADIX52) {  // (block engine: truncated / full; register CIOS at 1024 bits)
+        const size_t a = mpb::d52_workspace_bytes(count, bits, window), b = mpb::d52r_workspace_bytes(count, bits, window);
+        return a > b ? a : b;
+    }
     if (algo == MPB_ALGO_HYBRID) return mpb::hybrid_workspace_bytes(count, bits, window);
     const int C = block_of(L);
     const size_t kara = (size_t)mpb::kara_scratch_blocks_host(L / C, kara_levels(algo, L)) * C;
@@ -323,8 +326,10 @@ int mont_batch_modexp_ct(const uint32_t* N, const uint32_t* NP, const uint32_t* 
     if (redc == MPB_REDC_CIOS && (algo == MPB_ALGO_KARATSUBA || algo == MPB_ALGO_KARATSUBA2))
         return fail(MPB_EUNSUPPORTED, "CIOS (alg:8BlockMontRed) interleaves rows of a schoolbook product; "
                                       "Karatsuba needs MPB_REDC_FULL or MPB_REDC_TRUNCATED");
-    if ((algo == MPB_ALGO_RADIX52 || algo == MPB_ALGO_HYBRID) && redc == MPB_REDC_CIOS)
-        return fail(MPB_EUNSUPPORTED, "the radix-2^52 / hybrid paths have truncated and full REDC only");
+    if (algo == MPB_ALGO_HYBRID && redc == MPB_REDC_CIOS)
+        return fail(MPB_EUNSUPPORTED, "the hybrid path has truncated and full REDC only");
+    if (algo == MPB_ALGO_RADIX52 && redc == MPB_REDC_CIOS && !mpb::d52r_workspace_bytes(1, bits, window))
+        return fail(MPB_EUNSUPPORTED, "radix-2^52 CIOS (register-resident) exists for 1024-bit operands only");
     if (algo == MPB_ALGO_HYBRID && !mpb::hybrid_workspace_bytes(1, bits, window))
         return fail(MPB_EUNSUPPORTED, "the hybrid path serves 1921..2048-bit operands");
     if (algo == MPB_ALGO_RADIX52 && !mpb::d52_digits(bits))
@@ -352,6 +357,10 @@ int mont_batch_modexp_ct(const uint32_t* N, const uint32_t* NP, const uint32_t* 
     if (algo == MPB_ALGO_HYBRID) {
         mpb::launch_modexp_hybrid(N, NP, R2, base, exp, out, count, bits, window, redc == MPB_REDC_TRUNCATED,
                                   (uint32_t*)ws, (cudaStream_t)stream);
+        return check_launch();
+    }
+    if (algo == MPB_ALGO_RADIX52 && redc == MPB_REDC_CIOS) {
+        mpb::launch_modexp_d52r(N, R2, base, exp, out, count, bits, window, (uint32_t*)ws, (cudaStream_t)stream);
         return check_launch();
     }
     if (algo == MPB_ALGO_RADIX52) {

@@ -4,6 +4,7 @@
 // internal radix differs.
 #include "kernels.cuh"
 #include "mp_dfma.cuh"
+#include "mp_dfma_reg.cuh"
 
 #ifndef MPB_D52_MINB
 #define MPB_D52_MINB 3  // resident 128-thread CTAs per SM the radix-2^52 kernel is compiled for
@@ -152,6 +153,221 @@ __global__ void __launch_bounds__(kThreads, 3) k_modexp_hybrid(
     }
 }
 
+// Register-resident radix-2^52 exponentiation at 1024 bits (D = 20; mp_dfma_reg.cuh): alg:8FWExp on
+// alg:8BlockMontRed rows in the paper's radix with lazy FP64-split accumulators in registers.  The
+// 52-bit constants come from the 32-bit inputs in the kernel: n0' = -N^-1 mod 2^52 by Newton in 64-bit
+// integers, R52^2 = MontSqr52(MontMul52(R2_32, 2^k)), k = 130 D - 64 L (as k_modexp_d52).  Flat public
+// schedule, one MontMul call site; the a operand streams from a per-thread shared-memory slot.
+// Workspace (tiled, D/2 chunks per number): G (2^w numbers) | RR.
+template <int D>
+__global__ void __launch_bounds__(kThreads, 3) k_modexp_d52r(const uint32_t* __restrict__ N, const uint32_t* __restrict__ R2,
+                                                           const uint32_t* __restrict__ base, const uint32_t* __restrict__ exp,
+                                                           uint32_t* __restrict__ out, size_t count, int L, int bits, int w,
+                                                           uint32_t* ws) {
+    namespace d = d52;
+    const size_t k = tid_global();
+    if (k >= count) return;
+    constexpr int QD = D / 2;
+    const int nent = 1 << w;
+    const size_t cpad = (count + 31) & ~(size_t)31;
+    const ArrT G = tarr(ws, nent * QD, k);
+    const ArrT RRt = tarr(ws + cpad * (size_t)(nent * QD) * 4, QD, k);
+    extern __shared__ __align__(16) double smem_d[];
+    double* const sa = smem_d + threadIdx.x;  // double j of this thread at j * blockDim
+    const Arr Nn = arr(N, count, k), R2n = arr(R2, count, k), Bn = arr(base, count, k), On = arr(out, count, k);
+    // 32-bit word-sliced number -> D limbs of 52 bits (doubles), in registers
+    auto from32 = [&](const Arr& A, double (&x)[D]) {
+#pragma unroll
+        for (int j = 0; j < D; j++) {
+            const int b0 = 52 * j, q = b0 >> 5, r = b0 & 31;
+            uint64_t v = 0;
+#pragma unroll
+            for (int e = 0; e < 3; e++) {
+                const int wi = q + e;
+                uint32_t wv = 0;
+                if (wi < L) {
+                    const uint4 c = A.ld(wi >> 2);
+                    const int m = wi & 3;
+                    wv = m == 0 ? c.x : (m == 1 ? c.y : (m == 2 ? c.z : c.w));
+                }
+                const int sh = 32 * e - r;
+                if (sh >= 0) v |= sh < 64 ? (uint64_t)wv << sh : 0ull;
+                else v |= (uint64_t)(wv >> (-sh));
+            }
+            x[j] = d::to_d(v & d::kM52);
+        }
+    };
+    auto ld_num = [&](const ArrT& A, double (&x)[D]) {
+#pragma unroll
+        for (int q = 0; q < QD; q++) d::unpack2(A.ld(q), x[2 * q], x[2 * q + 1]);
+    };
+    auto st_num = [&](const ArrT& A, const double (&x)[D]) {
+#pragma unroll
+        for (int q = 0; q < QD; q++) A.st(q, d::pack2(x[2 * q], x[2 * q + 1]));
+    };
+    auto a_set = [&](const double (&x)[D]) {
+#pragma unroll
+        for (int j = 0; j < D; j++) sa[j * kThreads] = x[j];
+    };
+    auto aw = [&](int i) { return sa[i * kThreads]; };
+    double n[D];
+    from32(Nn, n);
+    double n0p;
+    {  // n0' = -N^-1 mod 2^52: Newton on the low 52 bits of N (an odd 64-bit integer)
+        const uint64_t n0 = d::limb_pat(n[0]) & d::kM52;
+        uint64_t x = n0;  // correct to 3 bits (odd n0: n0 * n0 = 1 mod 8)
+#pragma unroll
+        for (int it = 0; it < 5; it++) x = x * (2ull - n0 * x);
+        n0p = d::to_d((0ull - x) & d::kM52);
+    }
+    const int nwin = (bits + w - 1) / w;
+    auto window = [&](int win) {
+        const int pos = win * w, wi = pos >> 5, off = pos & 31;
+        uint32_t v = word_at(exp, count, k, wi) >> off;
+        if (off + w > 32 && wi + 1 < L) v |= word_at(exp, count, k, wi + 1) << (32 - off);
+        return v & ((1u << w) - 1u);
+    };
+    auto select = [&](uint32_t idx) {  // CT masked full-table scan into the a slot
+        uint4 acc[QD];
+#pragma unroll
+        for (int q = 0; q < QD; q++) acc[q] = make_uint4(0, 0, 0, 0);
+#pragma unroll 1
+        for (int e = 0; e < nent; e++) {
+            const uint32_t x = (uint32_t)e ^ idx;
+            const uint32_t m = 0u - ((x - 1u) >> 31);
+            const ArrT Ge = G.at(e * QD);
+#pragma unroll
+            for (int q = 0; q < QD; q++) {
+                const uint4 v = Ge.ld_stream(q);
+                acc[q].x |= v.x & m;
+                acc[q].y |= v.y & m;
+                acc[q].z |= v.z & m;
+                acc[q].w |= v.w & m;
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < QD; q++) {
+            double u, v;
+            d::unpack2(acc[q], u, v);
+            sa[(2 * q) * kThreads] = u;
+            sa[(2 * q + 1) * kThreads] = v;
+        }
+    };
+    // schedule: 0 Y = MontMul(R2_32, 2^k); 1 RR = MontSqr(Y); 2 G[0] = MontMul(RR, 1); 3 G[1] =
+    // MontMul(base, RR); 2 + e: G[e] = MontMul(G[e-1], G[1]); top window; windows; last MontMul(Y, 1)
+    double y[D];
+#pragma unroll
+    for (int j = 0; j < D; j++) y[j] = 0.0;
+    const int n_pre = nent + 2;
+    const int per_win = w + 1;
+    const int n_ops = n_pre + (nwin - 1) * per_win + 1;
+#pragma unroll 1
+    for (int op = 0; op < n_ops; op++) {
+        double b[D];
+        int kind = 0;  // 0: b = y, 1: b = one, 2: b loaded
+        const ArrT* store = nullptr;
+        ArrT dst = G;
+        if (op == 0) {
+            double x[D];
+            from32(R2n, x);
+            a_set(x);
+            const int kk = 130 * D - 64 * L;
+#pragma unroll
+            for (int j = 0; j < D; j++) b[j] = j == kk / 52 ? d::to_d(1ull << (kk % 52)) : 0.0;
+            kind = 2;
+        } else if (op == 1) {
+            a_set(y);
+            dst = RRt; store = &dst;
+        } else if (op == 2) {
+            double x[D];
+            ld_num(RRt, x);
+            a_set(x);
+            kind = 1;
+            dst = G; store = &dst;
+        } else if (op == 3) {
+            double x[D];
+            from32(Bn, x);
+            a_set(x);
+            ld_num(RRt, b);
+            kind = 2;
+            dst = G.at(QD); store = &dst;
+        } else if (op < n_pre) {
+            const int e = op - 2;
+            double x[D];
+            ld_num(G.at((e - 1) * QD), x);
+            a_set(x);
+            ld_num(G.at(QD), b);
+            kind = 2;
+            dst = G.at(e * QD); store = &dst;
+        } else if (op == n_ops - 1) {
+            a_set(y);
+            kind = 1;
+        } else {
+            const int r = (op - n_pre) % per_win, win = nwin - 2 - (op - n_pre) / per_win;
+            if (r < w) a_set(y);
+            else select(window(win));
+        }
+        if (kind == 0) {
+#pragma unroll
+            for (int j = 0; j < D; j++) b[j] = y[j];
+        } else if (kind == 1) {
+#pragma unroll
+            for (int j = 0; j < D; j++) b[j] = j == 0 ? 1.0 : 0.0;
+        }
+        d52r::montmul<D>(aw, b, n, n0p, y);
+        if (store) st_num(*store, y);
+        if (op == n_pre - 1) {  // after the table: Y = G[top window]
+            select(window(nwin - 1));
+#pragma unroll
+            for (int j = 0; j < D; j++) y[j] = aw(j);
+        }
+    }
+    // canonical [0, N): y - N if y >= N (y <= N after the final REDC), back to 32-bit limbs
+    uint64_t yl[D], dl[D];
+    uint64_t borrow = 0;
+#pragma unroll
+    for (int j = 0; j < D; j++) {
+        yl[j] = d::limb_pat(y[j]) & d::kM52;
+        const uint64_t v = yl[j] - (d::limb_pat(n[j]) & d::kM52) - borrow;
+        dl[j] = v & d::kM52;
+        borrow = (v >> 63) & 1ull;
+    }
+    const uint64_t m = 0ull - (borrow ^ 1ull);  // all ones: y >= N
+#pragma unroll
+    for (int j = 0; j < D; j++) yl[j] = (dl[j] & m) | (yl[j] & ~m);
+#pragma unroll 1
+    for (int q4 = 0; q4 < L / 4; q4++) {
+        uint32_t wv[4];
+#pragma unroll
+        for (int mm = 0; mm < 4; mm++) {
+            const int b0 = 32 * (4 * q4 + mm), j = b0 / 52, r = b0 - 52 * j;
+            uint64_t x = 0;
+#pragma unroll
+            for (int e = 0; e < D; e++) {  // (compile-time select of limbs j, j+1 without dynamic indexing)
+                if (e == j) x |= yl[e] >> r;
+                if (e == j + 1) x |= yl[e] << (52 - r);
+            }
+            wv[mm] = (uint32_t)x;
+        }
+        On.st(q4, make_uint4(wv[0], wv[1], wv[2], wv[3]));
+    }
+}
+
+size_t d52r_workspace_bytes(size_t count, int bits, int window) {
+    if (4 * ((bits + 127) / 128) != 32 || d52_digits(bits) != 20) return 0;
+    const size_t cpad = (count + 31) & ~(size_t)31;
+    return cpad * 10 * 16 * (size_t)((1 << window) + 1);
+}
+
+bool launch_modexp_d52r(const uint32_t* N, const uint32_t* R2, const uint32_t* base, const uint32_t* exp,
+                        uint32_t* out, size_t count, int bits, int window, uint32_t* ws, cudaStream_t s) {
+    if (!d52r_workspace_bytes(1, bits, window)) return false;
+    const unsigned g = (unsigned)((count + kThreads - 1) / kThreads);
+    k_modexp_d52r<20><<<g, kThreads, (size_t)kThreads * 20 * 8, s>>>(N, R2, base, exp, out, count, 32, bits, window,
+                                                                    ws);
+    return true;
+}
+
 // (C, NB) instances: 1024 (4, 5) D = 20; 2048 (8, 5) D = 40; 3072 (8, 8) D = 64; 4096 / 4108 (8, 10) D = 80
 int d52_digits(int bits) {
     const int L = 4 * ((bits + 127) / 128);
@@ -208,6 +424,7 @@ bool launch_modexp_hybrid(const uint32_t* N, const uint32_t* NP, const uint32_t*
 bool launch_modexp_d52(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
                        const uint32_t* exp, uint32_t* out, size_t count, int bits, int window, bool trunc,
                        uint32_t* ws, cudaStream_t s) {
+
     const int L = 4 * ((bits + 127) / 128);
     const unsigned g = (unsigned)((count + kThreads - 1) / kThreads);
     const size_t sm = (size_t)kThreads * 4 * 4 * 16;  // 2 buffers x 2 blocks x (C/2 <= 4) chunks

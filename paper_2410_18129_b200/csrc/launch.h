@@ -49,6 +49,11 @@ bool launch_modexp_d52(const uint32_t* N, const uint32_t* NP, const uint32_t* R2
                        const uint32_t* exp, uint32_t* out, size_t count, int bits, int window, bool trunc,
                        uint32_t* ws, cudaStream_t s);
 
+// register-resident radix-2^52 CIOS exponentiation at 1024 bits (inst_D52.cu, mp_dfma_reg.cuh)
+size_t d52r_workspace_bytes(size_t count, int bits, int window);
+bool launch_modexp_d52r(const uint32_t* N, const uint32_t* R2, const uint32_t* base, const uint32_t* exp,
+                        uint32_t* out, size_t count, int bits, int window, uint32_t* ws, cudaStream_t s);
+
 // hybrid 2048-bit exponentiation: 32-bit IMAD CTAs and radix-2^52 FP64 CTAs in one launch
 size_t hybrid_workspace_bytes(size_t count, int bits, int window);
 bool launch_modexp_hybrid(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,

@@ -485,6 +485,32 @@ def test_modexp_hybrid(mpb, count, redc):
     assert np.array_equal(h[idx], O.batch_modexp(base[idx], exp[idx], bits, N[idx]))
 
 
+@pytest.mark.parametrize("count,window", [(1, 5), (37, 5), (300, 4), (33, 1), (33, 6)])
+def test_modexp_radix52_cios_register_kernel(mpb, count, window):
+    """RADIX52 + CIOS at 1024 bits: the register-resident radix-2^52 CIOS kernel (mp_dfma_reg.cuh,
+    lazy FP64-split accumulators in registers) against the oracle, with edge operands."""
+    bits = 1024
+    L = I.limbs_for_bits(bits)
+    N, base, exp = I.modexp_inputs(config=1, count=count, bits=bits, dataset=500 + count + window)
+    if count >= 12:
+        N[0] = np.uint32(0xFFFFFFFF)
+        N[1] = 0
+        N[1, 0] = 1
+        N[1, L - 1] = np.uint32(1 << 31)
+        base[2] = 0
+        exp[2] = 0
+        base[3] = 0
+        base[4] = 0
+        base[4, 0] = 1
+        exp[5] = np.uint32(0xFFFFFFFF)
+        base[6] = I.to_limbs(I.from_limbs(N[6]) - 1, L)
+    dN = mpb.to_device(N)
+    Np, R2 = mpb.mont_batch_setup(dN, bits)
+    out = mpb.to_host(mpb.mont_batch_modexp_ct(dN, Np, R2, mpb.to_device(base), mpb.to_device(exp), bits,
+                                               window=window, redc=mpb.REDC_CIOS, algo=mpb.ALGO_RADIX52))
+    assert np.array_equal(out, O.batch_modexp(base, exp, bits, N))
+
+
 def test_modexp_radix52_rejects_unsupported(mpb):
     bits = 700
     N, base, exp = I.modexp_inputs(config=1, count=4, bits=bits)
