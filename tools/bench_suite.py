@@ -284,7 +284,7 @@ def main():
     if 8 in cfgs:  # radix-2^52 FP64 exponentiation and the hybrid launch, vs the IMAD path
         modexp_run(3, 2048, 1 << 18, args.reps, redcs=((1, "truncated"), (0, "full")), algo=4)
         modexp_run(3, 2048, 1 << 18, args.reps, redcs=((1, "truncated"),), algo=5)
-        modexp_run(2, 1024, 1 << 20, args.reps, redcs=((1, "truncated"),), algo=4)
+        modexp_run(2, 1024, 1 << 20, args.reps, redcs=((1, "truncated"), (2, "cios")), algo=4)
         modexp_run(4, 4096, 1 << 16, 1, redcs=((1, "truncated"),), algo=4)
     if 9 in cfgs:  # small 4096-bit batches: the 8 / 4 / 2-lane cooperative policy (north_star (b))
         for n in (2048, 8192, 16384):
