@@ -220,6 +220,85 @@ def test_truncated_reading_random_and_adversarial(bits):
     assert fired > 0  # the adversarial families really exercise the correction
 
 
+def _trunc_high_radix(q: int, N: int, D: int, w: int, T: int) -> int:
+    """Theorem 2's truncated high part in radix 2^w (reading A6/A7 with w-bit words; the radix-2^52
+    kernels, csrc/mp_dfma.cuh, use w = 52): products of weight >= D-1, hi halves of weight D-2,
+    carry out of column D-1 = floor(S / 2^w) + [S mod 2^w > K], K = (-T[D-1] - b) mod 2^w."""
+    M = (1 << w) - 1
+    qw = [(q >> (w * i)) & M for i in range(D)]
+    nw = [(N >> (w * i)) & M for i in range(D)]
+    S, high = 0, 0
+    for i in range(D):
+        for j in range(D):
+            p = qw[i] * nw[j]
+            lo, hi = p & M, p >> w
+            if i + j == D - 1:
+                S += lo
+            if i + j == D - 2:
+                S += hi
+            if i + j >= D:
+                high += lo << (w * (i + j - D))
+            if i + j >= D - 1:
+                high += hi << (w * (i + j + 1 - D))
+    b = 1 if T % (1 << (w * (D - 1))) else 0
+    K = (-((T >> (w * (D - 1))) & M) - b) & M
+    return high + (S >> w) + (1 if (S & M) > K else 0)
+
+
+@pytest.mark.parametrize("bits,D", [(1024, 20), (2048, 40)])
+def test_truncated_reading_radix52(bits, D):
+    """The radix-2^52 reading of Theorem 2 (DESIGN 3.2, the RADIX52 kernels) equals floor(qN/R),
+    R = 2^(52D), on random T and on a forced-wrap family built in radix 2^52 (S mod 2^52 =
+    2^52-1-k), where the correction term is needed; dropping it fails there."""
+    w = 52
+    R = 1 << (w * D)
+    M = (1 << w) - 1
+    fired = 0
+    for _ in range(3):
+        N = RNG.getrandbits(bits) | 1 | (1 << (bits - 1))
+        Np = (-pow(N, -1, R)) % R
+        cases = [RNG.randrange(N * R) for _ in range(3)]
+        for k in (0, 1, 2):  # forced wrap: choose q's top limb so S mod 2^52 = 2^52 - 1 - k
+            q = RNG.randrange(R) & ~(M << (w * (D - 1)))
+            qw = [(q >> (w * i)) & M for i in range(D)]
+            nw = [(N >> (w * i)) & M for i in range(D)]
+            rest = sum((qw[i] * nw[D - 1 - i]) & M for i in range(D - 1)) + \
+                sum((qw[i] * nw[D - 2 - i]) >> w for i in range(D - 1))
+            top = (((M - k) - rest) * pow(nw[0], -1, 1 << w)) & M
+            q |= top << (w * (D - 1))
+            cases.append((-q * N) % R + RNG.randrange(N) * R)
+        for T in cases:
+            q = ((T % R) * Np) % R
+            got = _trunc_high_radix(q, N, D, w, T)
+            assert got == (q * N) // R
+            C = T // R + got + (1 if T % R else 0)
+            assert C == (T + q * N) // R  # Theorem 1 in radix 2^52
+            # is the correction term what made it exact?
+            S_lo_gt_K = got - _trunc_high_radix_no_corr(q, N, D, w)
+            fired += S_lo_gt_K
+    assert fired > 0
+
+
+def _trunc_high_radix_no_corr(q: int, N: int, D: int, w: int) -> int:
+    M = (1 << w) - 1
+    qw = [(q >> (w * i)) & M for i in range(D)]
+    nw = [(N >> (w * i)) & M for i in range(D)]
+    S, high = 0, 0
+    for i in range(D):
+        for j in range(D):
+            p = qw[i] * nw[j]
+            lo, hi = p & M, p >> w
+            if i + j == D - 1:
+                S += lo
+            if i + j == D - 2:
+                S += hi
+            if i + j >= D:
+                high += lo << (w * (i + j - D))
+            if i + j >= D - 1:
+                high += hi << (w * (i + j + 1 - D))
+    return high + (S >> w)
+
+
 # --------------------------------------------------------------------- modexp
 def test_modexp_exhaustive_tiny():
     for N in range(3, 1 << 6, 2):
