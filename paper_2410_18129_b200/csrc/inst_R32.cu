@@ -289,11 +289,10 @@ bool launch_modexp_rtr(const uint32_t* N, const uint32_t* NP, const uint32_t* R2
     if (4 * ((bits + 127) / 128) != 32) return false;
     const unsigned g = (unsigned)((count + kThreads - 1) / kThreads);
     const size_t sm = (size_t)kThreads * 32 * 4 * 4;  // a, N, N', T_high
-    static bool attr = [] {
-        return cudaFuncSetAttribute(k_modexp_rtr<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024) ==
-               cudaSuccess;
-    }();
-    (void)attr;
+    // 64 KB of dynamic shared memory needs the opt-in on every device the kernel runs on (per call:
+    // a static would set it for the first device only)
+    if (cudaFuncSetAttribute(k_modexp_rtr<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
+        return false;
     k_modexp_rtr<32><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, bits, window, ws);
     return true;
 }

@@ -218,7 +218,6 @@ MPB_DEVI void engine(int ph, const ArrT& AX, const ArrT& AY, const ArrT& DST, co
         carry = (orlo != 0u || tl1 != 0ull) ? 1ull : 0ull;  // c_add = [T mod R != 0]
         K = (0ull - tl1 - b) & kM52;                          // K = (-T[D-1] - b) mod 2^52
     }
-    constexpr uint32_t kTile = QB * 512u;
     auto issue = [&](int kk, int ss, int buf) {
         const uint32_t base = sg.base + (uint32_t)(buf * 2 * QB) * kStageCS;
         const char* bx = reinterpret_cast<const char*>(AX.addr(ss * QB));
@@ -231,7 +230,6 @@ MPB_DEVI void engine(int ph, const ArrT& AX, const ArrT& AY, const ArrT& DST, co
         }
         cp_commit();
     };
-    (void)kTile;
     int k = k0, s = k0 - NB + 1 > 0 ? k0 - NB + 1 : 0;
     int s_hi = sqr ? (k >> 1) : (k < NB - 1 ? k : NB - 1);
     issue(k, s, 0);

@@ -84,8 +84,6 @@ MPB_DEVI void montmul(const AW& aw, const double (&b)[D], const double (&n)[D], 
     // normalise positions D .. 2D (the last row left its top halves at 2D)
 #pragma unroll
     for (int k = 0; k < D; k++) {
-        constexpr int dummy = 0;
-        (void)dummy;
         const uint64_t v = Y[D + k] - bias_pos<D>(D + k, D) + cin;
         out[k] = to_d(v & kM52);
         cin = v >> 52;
