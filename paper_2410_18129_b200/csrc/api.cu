@@ -259,7 +259,8 @@ static int mont_op(const uint32_t* a, const uint32_t* b, const uint32_t* N, cons
     if (c == a || c == b || c == N || c == NP) return fail(MPB_EINVAL, "output aliases an input");
     if (ws_bytes < mont_batch_workspace(count, bits)) return fail(MPB_EINVAL, "workspace too small");
     if (redc == MPB_REDC_CIOS && L == 32 && reg_policy() != 0) {  // 1024 bits: register-resident CIOS
-        mpb::launch_mont_mul_reg(a, sqr ? a : b, N, NP, c, count, bits, (cudaStream_t)stream);
+        if (!mpb::launch_mont_mul_reg(a, sqr ? a : b, N, NP, c, count, bits, (cudaStream_t)stream))
+            return fail(MPB_ECUDA, "launch_mont_mul_reg: launch refused");
         return check_launch();
     }
     return dispatch_L(L, [&](auto Ci, int nb) {
@@ -345,27 +346,32 @@ int mont_batch_modexp_ct(const uint32_t* N, const uint32_t* NP, const uint32_t* 
         return fail(MPB_EINVAL, "workspace too small");
     if (redc == MPB_REDC_CIOS && L == 32 && algo <= MPB_ALGO_SCHOOLBOOK && reg_policy() != 0) {
         // 1024 bits, CIOS: the register-resident exponentiation (inst_R32.cu)
-        mpb::launch_modexp_reg(N, NP, R2, base, exp, out, count, bits, window, (uint32_t*)ws, (cudaStream_t)stream);
+        if (!mpb::launch_modexp_reg(N, NP, R2, base, exp, out, count, bits, window, (uint32_t*)ws, (cudaStream_t)stream))
+            return fail(MPB_ECUDA, "launch_modexp_reg: launch refused");
         return check_launch();
     }
     if (redc == MPB_REDC_TRUNCATED && L == 32 && algo <= MPB_ALGO_SCHOOLBOOK && reg_policy() == 2) {
         // 1024 bits, truncated: the register-resident truncated exponentiation (inst_R32.cu; opt-in
         // MPB_REG=2 until measured)
-        mpb::launch_modexp_rtr(N, NP, R2, base, exp, out, count, bits, window, (uint32_t*)ws, (cudaStream_t)stream);
+        if (!mpb::launch_modexp_rtr(N, NP, R2, base, exp, out, count, bits, window, (uint32_t*)ws, (cudaStream_t)stream))
+            return fail(MPB_ECUDA, "launch_modexp_rtr: launch refused");
         return check_launch();
     }
     if (algo == MPB_ALGO_HYBRID) {
-        mpb::launch_modexp_hybrid(N, NP, R2, base, exp, out, count, bits, window, redc == MPB_REDC_TRUNCATED,
-                                  (uint32_t*)ws, (cudaStream_t)stream);
+        if (!mpb::launch_modexp_hybrid(N, NP, R2, base, exp, out, count, bits, window, redc == MPB_REDC_TRUNCATED,
+                                  (uint32_t*)ws, (cudaStream_t)stream))
+            return fail(MPB_ECUDA, "launch_modexp_hybrid: launch refused");
         return check_launch();
     }
     if (algo == MPB_ALGO_RADIX52 && redc == MPB_REDC_CIOS) {
-        mpb::launch_modexp_d52r(N, R2, base, exp, out, count, bits, window, (uint32_t*)ws, (cudaStream_t)stream);
+        if (!mpb::launch_modexp_d52r(N, R2, base, exp, out, count, bits, window, (uint32_t*)ws, (cudaStream_t)stream))
+            return fail(MPB_ECUDA, "launch_modexp_d52r: launch refused");
         return check_launch();
     }
     if (algo == MPB_ALGO_RADIX52) {
-        mpb::launch_modexp_d52(N, NP, R2, base, exp, out, count, bits, window, redc == MPB_REDC_TRUNCATED,
-                               (uint32_t*)ws, (cudaStream_t)stream);
+        if (!mpb::launch_modexp_d52(N, NP, R2, base, exp, out, count, bits, window, redc == MPB_REDC_TRUNCATED,
+                               (uint32_t*)ws, (cudaStream_t)stream))
+            return fail(MPB_ECUDA, "launch_modexp_d52: launch refused");
         return check_launch();
     }
     return dispatch_L(L, [&](auto Ci, int nb) {
