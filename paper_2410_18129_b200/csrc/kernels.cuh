@@ -210,6 +210,9 @@ __global__ void __launch_bounds__(kThreads, min_blocks<C>()) k_mont_redc_tiled(
 #ifndef MPB_TILE
 #define MPB_TILE 1
 #endif
+#ifndef MPB_ONEWAVE_C12
+#define MPB_ONEWAVE_C12 1  // 4108 bits: the 4-CTA one-wave instance too (measured, DESIGN 5.3b)
+#endif
 // tiled for the compile-time block counts (the hot sizes); the generic-NB kernels run measurably
 // slower with it (1536 / 2560 / 4108 bits: 5-20 %) and keep the word-sliced workspace
 __host__ __device__ constexpr bool modexp_tiled(int KLEV, bool TMA, int NBT) {
@@ -723,7 +726,7 @@ void Launch<C>::modexp(const uint32_t* N, const uint32_t* NP, const uint32_t* R2
                 if (levels >= 2) return go(std::integral_constant<int, 2>{});
                 if (levels == 1) return go(std::integral_constant<int, 1>{});
             }
-            if constexpr (C == 16 && NBT == 8) {
+            if constexpr ((C == 16 && NBT == 8) || (C == 12 && NBT == 11 && MPB_ONEWAVE_C12)) {
                 // 4096 bits: a batch that needs two waves at 3 CTAs per SM but fits ONE wave at 4
                 // (128 registers, a few spills) runs the 4-CTA instance -- config 4 (2^16 operands,
                 // 1.15 waves at 3 CTAs): 46.1 K vs 44.3 K/s measured; many-wave batches keep 3 CTAs

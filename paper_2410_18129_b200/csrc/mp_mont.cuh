@@ -256,9 +256,12 @@ enum { PH_MUL = 0, PH_SQR = 1, PH_Q = 2, PH_HI = 3 };
 #ifndef MPB_KARA_MIN_NB
 #define MPB_KARA_MIN_NB 6
 #endif
+#ifndef MPB_KARA_C12
+#define MPB_KARA_C12 1  // C = 12 blocks (4108 / 4154 bits): measured +1.4 % alone, +10.5 % with one wave
+#endif
 template <int C>
 __host__ __device__ constexpr bool kara_blocks() {
-    return MPB_KARA_BLOCK && C == 16;
+    return MPB_KARA_BLOCK && (C == 16 || (C == 12 && MPB_KARA_C12));
 }
 enum { OP_MUL = 0, OP_MUL2 = 1, OP_SQR = 2, OP_LO = 3, OP_HI = 4 };
 
