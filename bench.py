@@ -75,12 +75,12 @@ KARA_MIN_NB = 6  # csrc/mp_mont.cuh: full 16-limb blocks by register Karatsuba f
 def kara_saved_imad(L: int, redc: int) -> dict:
     """IMAD the engine's register-Karatsuba blocks (mp_block.cuh acc_kara: 3 half-size products,
     3C^2/4 instead of C^2 word products) do NOT execute per operation, for the sizes where the engine
-    uses them (C = 16, NB = L/16 >= KARA_MIN_NB; truncated or full REDC).  Kara blocks: PH_MUL all NB^2,
+    uses them (C = 16 or 12, NB = L/C >= KARA_MIN_NB; truncated or full REDC).  Kara blocks: PH_MUL all NB^2,
     PH_SQR the NB(NB-1)/2 off-diagonal ones, PH_Q the NB(NB-1)/2 below its top column, PH_HI the
-    NB(NB-1)/2 above column NB-1 (truncated) or all NB^2 (full); each saves 16^2/4 products = 128 IMAD."""
+    NB(NB-1)/2 above column NB-1 (truncated) or all NB^2 (full); each saves C^2/4 products (C^2/2 IMAD)."""
     C = block_for(L)
     NB = L // C
-    if redc == 2 or C != 16 or NB < KARA_MIN_NB:
+    if redc == 2 or C not in (16, 12) or NB < KARA_MIN_NB:
         return {"mul": 0, "sqr": 0, "redc": 0}
     tri = NB * (NB - 1) // 2
     hi = tri if redc else NB * NB
