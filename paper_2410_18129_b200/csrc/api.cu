@@ -309,7 +309,9 @@ size_t mont_batch_modexp_ct_workspace(size_t count, int bits, int window, int al
     }
     if (algo == MPB_ALGO_HYBRID) return mpb::hybrid_workspace_bytes(count, bits, window);
     const int C = block_of(L);
-    const size_t kara = (size_t)mpb::kara_scratch_blocks_host(L / C, kara_levels(algo, L)) * C;
+    const int lev = kara_levels(algo, L);
+    // Karatsuba product scratch, plus the truncated-Karatsuba REDC's 6 NB blocks (mp_kara.cuh)
+    const size_t kara = (size_t)mpb::kara_scratch_blocks_host(L / C, lev) * C + (lev > 0 ? (size_t)6 * L : 0);
     // word-sliced layout (Karatsuba products, TMA tiles): G | Y | T | Q | S | scratch, stride count;
     // warp-tiled layout (the default path): G | Y | T | Q | S | N | N' over count rounded up to 32
     const size_t sliced = count * ((size_t)L * (size_t)((1 << window) + 5) + kara);

@@ -161,6 +161,170 @@ namespace mpb {
 // Montgomery operation whose product phase (T = X*B or X^2) uses KLEV levels of block Karatsuba
 // (Karatsuba inside MontMul/MontSqr); the reduction phases stay on the engine.
 // KS: kara_scratch_blocks(NB, KLEV) blocks of scratch.  KLEV = 0 is mont_op.
+// ------------------------------------------------ truncated-Karatsuba REDC (f1)
+// floor(x*y / 2^(32 C nb)) for nb-block x, y, given K = word C*nb-1 of (x*y mod 2^(32 C nb)):
+// Theorem 2's truncated high part (corners of block column nb-2, truncated high blocks of column
+// nb-1, the exact carry [S mod 2^32 > K], full blocks above) -- PH_HI's walk without T, emit, select.
+template <int C>
+__device__ __noinline__ void trunc_high_product(int nb, Arr X, Arr Y, uint32_t K, Arr DST) {
+    uint32_t W[2 * C + 1];
+    w_zero<C>(W);
+#pragma unroll 1
+    for (int s = 0; s + 2 <= nb; s++) {
+        const uint32_t xw = X.ld(s * (C / 4) + C / 4 - 1).w, yw = Y.ld((nb - 2 - s) * (C / 4) + C / 4 - 1).w;
+        asm volatile("mad.hi.cc.u32 %0, %2, %3, %0;\n\taddc.u32 %1, %1, 0;" : "+r"(W[0]), "+r"(W[1]) : "r"(xw), "r"(yw));
+    }
+#pragma unroll 1
+    for (int s = 0; s < nb; s++) {
+        uint32_t x[C], y[C];
+        ldb<C>(X, s, x);
+        ldb<C>(Y, nb - 1 - s, y);
+        acc_hi<C>(W, x, y);
+    }
+    {
+        const uint32_t corr = W[0] > K ? 1u : 0u;
+#pragma unroll
+        for (int i = 0; i < 2 * C; i++) W[i] = W[i + 1];
+        W[2 * C] = 0;
+        add_first(W[0], corr);
+#pragma unroll
+        for (int i = 1; i <= C; i++) add_next(W[i], 0u);
+        absorb(W[C + 1]);
+    }
+#pragma unroll 1
+    for (int k = nb; k <= 2 * nb - 2; k++) {
+#pragma unroll 1
+        for (int s = k - nb + 1; s < nb; s++) {
+            uint32_t x[C], y[C];
+            ldb<C>(X, s, x);
+            ldb<C>(Y, k - s, y);
+            acc_mul<C>(W, x, y);
+        }
+        stb<C>(DST, k - nb, W);
+        w_shift<C>(W);
+    }
+    stb<C>(DST, nb - 1, W);
+}
+
+// The high part of the Montgomery reduction, floor(q N / R), by the paper's truncated Karatsuba
+// (trunc(A B) = 2^t (D2l + D1h - D0h - D2h) + 2^(3t/2) D2h, computed "with the same kind
+// of carry evaluation" as the truncated schoolbook), in the subtractive form (reading A4) with the
+// exact carries derived from the known low half Lam = q N mod R = (-T) mod R:
+//   halves of h = NB/2 blocks, X = 2^(32 C h):  D2 = q1 N1 (full), D0h = floor(q0 N0 / X) (Theorem 2,
+//   K0 = word of Lam_l), Dm = |q0 - q1| |N0 - N1|, sigma = +1 iff the two differences have the same
+//   sign (mid = D0 + D2 - sigma Dm), V = D0h + Lam_l + D2l - Lam_h, Dml = sigma V mod X,
+//   Dmh = floor(Dm / X) (Theorem 2, K = top word of Dml), c = floor(V / X) + [sigma = -1, V mod X != 0],
+//   floor(q N / R) = D2 + D0h + D2h - sigma Dmh + c.
+// Then C = floor(T/R) + that + c_add, D = C - N, canonical by a mask (as PH_HI).  Block products:
+// h^2 + 2 (h^2/2 + h) -- the truncated schoolbook high part's (2h)^2/2 + 2h; the linear passes are the
+// extra cost.  NB even.  S: 6 NB blocks of scratch (word-sliced, like T).
+template <int C>
+__device__ __noinline__ void kara_trunc_high(int NB, Arr T, Arr Q, Arr N, Arr OUT, Arr S, Stage sg) {
+    constexpr int Q4 = C / 4;
+    const int h = NB / 2;
+    const Arr LAM = S, D2 = S.at(NB * Q4), D0H = S.at(2 * NB * Q4), DML = S.at((2 * NB + h) * Q4),
+              DQ = S.at((2 * NB + 2 * h) * Q4), DN = S.at((2 * NB + 3 * h) * Q4), DMH = S.at((2 * NB + 4 * h) * Q4);
+    // Lam = (0 - T_low) mod R; c_add = [T mod R != 0] = the final borrow
+    uint32_t bw = 0;
+#pragma unroll 1
+    for (int j = 0; j < NB; j++) {
+        uint32_t t[C], z[C];
+        ldb<C>(T, j, t);
+#pragma unroll
+        for (int i = 0; i < C; i++) z[i] = 0;
+        bc_restore(bw);
+#pragma unroll
+        for (int i = 0; i < C; i++) sub_next(z[i], t[i]);
+        bw = bc_save();
+        stb<C>(LAM, j, z);
+    }
+    const uint32_t cadd = bw;
+    engine_product<C>(false, h, Q.at(h * Q4), N.at(h * Q4), D2, sg);                 // D2 = q1 N1
+    trunc_high_product<C>(h, Q, N, LAM.ld((h * C - 1) / 4).w, D0H);                   // D0h
+    const uint32_t sq = kara_absdiff<C>(Q, h, h, DQ), sn = kara_absdiff<C>(N, h, h, DN);
+    const int64_t sigma = sq == sn ? 1 : -1;  // (a mask-like value: no branch depends on it)
+    // V = D0h + Lam_l + D2_l - Lam_h (signed carry), Dml = sigma V mod X
+    int64_t cv = 0;
+    uint32_t vnz = 0;
+#pragma unroll 1
+    for (int j = 0; j < h; j++) {
+        uint32_t a[C], b[C], d[C], e[C], v[C];
+        ldb<C>(D0H, j, a);
+        ldb<C>(LAM, j, b);
+        ldb<C>(D2, j, d);
+        ldb<C>(LAM, h + j, e);
+#pragma unroll
+        for (int i = 0; i < C; i++) {
+            const int64_t sm = (int64_t)a[i] + (int64_t)b[i] + (int64_t)d[i] - (int64_t)e[i] + cv;
+            v[i] = (uint32_t)sm;
+            cv = sm >> 32;  // arithmetic: floor
+            vnz |= v[i];
+        }
+        stb<C>(DML, j, v);
+    }
+    {  // Dml = sigma == -1 ? (-V mod X) : V  (two's complement under a mask)
+        const uint32_t m = sigma < 0 ? 0xFFFFFFFFu : 0u;
+        uint32_t cy = m & 1u;
+#pragma unroll 1
+        for (int j = 0; j < h; j++) {
+            uint32_t v[C];
+            ldb<C>(DML, j, v);
+#pragma unroll
+            for (int i = 0; i < C; i++) v[i] ^= m;
+            cc_restore(cy);
+#pragma unroll
+            for (int i = 0; i < C; i++) add_next(v[i], 0u);
+            cy = cc_save();
+            stb<C>(DML, j, v);
+        }
+    }
+    const int64_t c = cv + ((sigma < 0 && vnz != 0u) ? 1 : 0);
+    trunc_high_product<C>(h, DQ, DN, DML.ld((h * C - 1) / 4).w, DMH);                 // Dmh
+    // H = D2 + (D0h + D2h - sigma Dmh + c); C = T_hi + H + c_add into T[NB..2NB), D = C - N into OUT
+    int64_t ch = c;
+    uint32_t cyc = cadd, borrow = 0;
+#pragma unroll 1
+    for (int j = 0; j < NB; j++) {
+        uint32_t d2[C], th[C], n[C], hv[C];
+        ldb<C>(D2, j, d2);
+        ldb<C>(T, NB + j, th);
+        ldb<C>(N, j, n);
+        if (j < h) {
+            uint32_t a[C], e[C], f[C];
+            ldb<C>(D0H, j, a);
+            ldb<C>(D2, h + j, e);
+            ldb<C>(DMH, j, f);
+#pragma unroll
+            for (int i = 0; i < C; i++) {
+                const int64_t sm = (int64_t)d2[i] + (int64_t)a[i] + (int64_t)e[i] - sigma * (int64_t)f[i] + ch;
+                hv[i] = (uint32_t)sm;
+                ch = sm >> 32;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < C; i++) {
+                const int64_t sm = (int64_t)d2[i] + ch;
+                hv[i] = (uint32_t)sm;
+                ch = sm >> 32;
+            }
+        }
+        cc_restore(cyc);  // C block = T_hi block + H block + carry
+#pragma unroll
+        for (int i = 0; i < C; i++) add_next(th[i], hv[i]);
+        cyc = cc_save();
+        stb<C>(T, NB + j, th);
+        bc_restore(borrow);  // D block = C block - N block
+#pragma unroll
+        for (int i = 0; i < C; i++) sub_next(th[i], n[i]);
+        borrow = bc_save();
+        stb<C>(OUT, j, th);
+    }
+    final_select<C>(NB, T, OUT, cyc, borrow);
+}
+
+// Scratch blocks of kara_trunc_high for nb blocks (6 nb; mirrored by kara_redc_scratch_blocks_host).
+__host__ __device__ constexpr int kara_redc_scratch_blocks(int nb) { return 6 * nb; }
+
 template <int C, bool TRUNC, int KLEV, class AR = Arr>
 MPB_DEVI void mont_op_k(int mode, int NB, const AR& X, const AR& B, const AR& N, const AR& NP, const AR& T,
                         const AR& Q, const AR& OUT, const AR& KS, const Stage& sg) {
@@ -168,7 +332,14 @@ MPB_DEVI void mont_op_k(int mode, int NB, const AR& X, const AR& B, const AR& N,
         mont_op<C, TRUNC>(mode, NB, X, B, N, NP, T, Q, OUT, sg);
     } else {
         if (mode != MODE_REDC) kmul<C, KLEV>(mode == MODE_SQR, NB, X, B, T, KS, sg);
-        mont_op<C, TRUNC>(MODE_REDC, NB, X, B, N, NP, T, Q, OUT, sg);
+        if (TRUNC && (NB & 1) == 0 && NB >= 2) {
+            // q = T N' mod R (schoolbook low half, PH_Q), then the truncated-Karatsuba high part
+            uint32_t ol[2] = {0u, 0u};
+            engine_call<C, true>(PH_Q, NB, T, NP, Q, T, N, OUT, ol, sg);
+            kara_trunc_high<C>(NB, T, Q, N, OUT, KS.at(kara_scratch_blocks(NB, KLEV) * (C / 4)), sg);
+        } else {
+            mont_op<C, TRUNC>(MODE_REDC, NB, X, B, N, NP, T, Q, OUT, sg);
+        }
     }
 }
 

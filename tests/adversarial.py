@@ -74,3 +74,44 @@ def redc_family(rng: random.Random, N: int, L: int, per_family: int = 4) -> list
     for t in t_delta(N, L):
         out.append(("delta", t))
     return out
+
+
+# ----------------------------------------------- truncated-Karatsuba REDC (f1) families
+def craft_half(rng: random.Random, y: int, H: int, k: int) -> int:
+    """x (H words) with column H-1 of x*y forced: S mod 2^32 = 2^32-1-k (S = lo halves of weight H-1 +
+    hi halves of weight H-2, the Theorem-2 column of an H-word product).  Needs y odd."""
+    M = (1 << 32) - 1
+    x = rng.getrandbits(32 * H) & ~(M << (32 * (H - 1)))
+    xw = [(x >> (32 * i)) & M for i in range(H)]
+    yw = [(y >> (32 * i)) & M for i in range(H)]
+    rest = sum((xw[i] * yw[H - 1 - i]) & M for i in range(H - 1)) + \
+        sum((xw[i] * yw[H - 2 - i]) >> 32 for i in range(H - 1))
+    top = (((M - k) - rest) * pow(yw[0], -1, 1 << 32)) & M
+    return x | (top << (32 * (H - 1)))
+
+
+def t_kara_trunc(rng: random.Random, N: int, L: int, k0: int, km: int, below_n: bool = False):
+    """A REDC input T whose q = T N' mod R makes BOTH half-level corrections of the truncated-
+    Karatsuba REDC necessary: q0 * N0 and |q0 - q1| * |N0 - N1| each get a forced-wrap Theorem-2
+    column (halves of H = L/2 words).  below_n: T < N (a valid operand in the R^2 position).
+    Returns None when N's halves do not allow it (N0 or |N0 - N1| even)."""
+    H = L // 2
+    X = 1 << (32 * H)
+    R = X * X
+    n0, n1 = N % X, N // X
+    dn = abs(n0 - n1)
+    if n0 % 2 == 0 or dn % 2 == 0:
+        return None
+    for _ in range(2000):
+        q0 = craft_half(rng, n0, H, k0)
+        dq = craft_half(rng, dn, H, km)
+        if dq > q0:
+            continue
+        q = q0 + (q0 - dq) * X
+        t_lo = (-q * N) % R
+        if below_n:
+            if t_lo < N:
+                return t_lo
+            continue
+        return t_lo + rng.randrange(N) * R
+    return None

@@ -15,7 +15,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from adversarial import redc_family, t_gamma
+from adversarial import redc_family, t_gamma, t_kara_trunc
 from paper_2410_18129_b200 import inputs as I
 
 pytestmark = pytest.mark.gpu
@@ -689,7 +689,7 @@ def test_sharded_slices_match_whole_batch(mpb):
 
 
 @pytest.mark.parametrize("algo", [2, 3])
-@pytest.mark.parametrize("bits", [1536, 3072, 4096, 4108])
+@pytest.mark.parametrize("bits", [1536, 3072, 4096, 4108, 5120])
 def test_modexp_karatsuba_products(mpb, bits, algo):
     """Karatsuba (1 and 2 levels) in the product phase of every MontMul/MontSqr."""
     count = 5
@@ -699,6 +699,40 @@ def test_modexp_karatsuba_products(mpb, bits, algo):
     out = mpb.to_host(mpb.mont_batch_modexp_ct(dN, Np, R2, mpb.to_device(base), mpb.to_device(exp), bits,
                                                window=5, algo=algo))
     assert np.array_equal(out, O.batch_modexp(base, exp, bits, N))
+
+
+@pytest.mark.parametrize("algo", [2, 3])
+def test_truncated_karatsuba_redc_crafted(mpb, algo):
+    """The truncated-Karatsuba REDC (mp_kara.cuh kara_trunc_high, used by the Karatsuba
+    exponentiation at 4096 bits) on inputs that force BOTH half-level Theorem-2 corrections
+    (tests/adversarial.py t_kara_trunc, pinned in test_oracle): the crafted T stands in the R^2
+    position, so the exponentiation's first operation REDC(R2) needs them.  Every operand equals
+    the exact schedule and the schoolbook kernel's output on the same inputs."""
+    bits, w, count = 4096, 5, 6
+    L = I.limbs_for_bits(bits)
+    H = L // 2
+    R = 1 << (32 * L)
+    N, base, exp = I.modexp_inputs(config=4, count=count, bits=bits, dataset=11)
+    N[:, H] &= np.uint32(0xFFFFFFFE)  # N1 even, N0 odd: |N0 - N1| odd (the construction needs it)
+    Ns = ints(N)
+    Bs = [b % n for b, n in zip(ints(base), Ns)]
+    base = I.ints_to_array(Bs, L)
+    Es = ints(exp)
+    rng = random.Random(4096 + algo)
+    rho = []
+    for k, n in enumerate(Ns):
+        t = t_kara_trunc(rng, n, L, k % 3, (k + 1) % 3, below_n=True)
+        assert t is not None
+        rho.append(t)
+    dN, dB, dE = (mpb.to_device(x) for x in (N, base, exp))
+    Np, _ = mpb.mont_batch_setup(dN, bits)
+    dR = mpb.to_device(I.ints_to_array(rho, L))
+    out = mpb.to_host(mpb.mont_batch_modexp_ct(dN, Np, dR, dB, dE, bits, w, redc=mpb.REDC_TRUNCATED, algo=algo))
+    ref = mpb.to_host(mpb.mont_batch_modexp_ct(dN, Np, dR, dB, dE, bits, w, redc=mpb.REDC_TRUNCATED,
+                                               algo=mpb.ALGO_SCHOOLBOOK))
+    assert np.array_equal(out, ref)
+    for k in (0, count - 1):
+        assert I.from_limbs(out[k]) == _schedule_modexp(Bs[k], Es[k], Ns[k], rho[k], L, bits, w), k
 
 
 # ----------------------------------------------------------------- CRT-RSA (f4)

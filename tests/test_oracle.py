@@ -299,6 +299,65 @@ def _trunc_high_radix_no_corr(q: int, N: int, D: int, w: int) -> int:
     return high + (S >> w)
 
 
+def _trunc_karatsuba_high(T: int, q: int, N: int, L: int) -> int:
+    """The truncated-Karatsuba high part of the REDC (reading in DESIGN 5.7b), as
+    csrc/mp_kara.cuh kara_trunc_high computes it, word level: halves of H = L/2 words, Lam = -T mod R
+    known, D0h and Dmh by Theorem 2 with K from Lam's low half and from Dml."""
+    H = L // 2
+    X = 1 << (32 * H)
+    R = X * X
+    lam = (-T) % R
+    lam_l, lam_h = lam % X, lam // X
+    q0, q1, n0, n1 = q % X, q // X, N % X, N // X
+    D2 = q1 * n1
+    D2l, D2h = D2 % X, D2 // X
+    # _trunc_high_radix derives K = word H-1 of (-Targ mod X); here the known low half is Lam_l itself
+    D0h = _trunc_high_radix(q0, n0, H, 32, (-lam_l) % X)
+    sigma = 1 if (q0 >= q1) == (n0 >= n1) else -1
+    V = D0h + lam_l + D2l - lam_h
+    Dml = V % X if sigma == 1 else (-V) % X
+    Dmh = _trunc_high_radix(abs(q0 - q1), abs(n0 - n1), H, 32, (-Dml) % X)
+    c = V // X + (1 if sigma == -1 and V % X else 0)
+    return D2 + D0h + D2h - sigma * Dmh + c
+
+
+@pytest.mark.parametrize("bits", [512, 1024, 2048, 4096])
+def test_truncated_karatsuba_reading(bits):
+    """The truncated-Karatsuba REDC reading equals floor(qN/R) on random T, on T mod R = 0, and on
+    the adversarial family of tests/adversarial.py t_kara_trunc, which forces BOTH half-level
+    Theorem-2 corrections (dropping either one fails there)."""
+    from adversarial import t_kara_trunc
+
+    L = I.limbs_for_bits(bits)
+    R = 1 << (32 * L)
+    H = L // 2
+    X = 1 << (32 * H)
+    crafted = 0
+    for _ in range(6):
+        N = RNG.getrandbits(bits) | 1 | (1 << (bits - 1))
+        Np = (-pow(N, -1, R)) % R
+        Ts = [RNG.randrange(N * R), RNG.randrange(N) * R]
+        for k0, km in ((0, 0), (1, 2), (2, 1)):
+            t = t_kara_trunc(RNG, N, L, k0, km)
+            if t is not None:
+                Ts.append(t)
+                crafted += 1
+        for T in Ts:
+            q = ((T % R) * Np) % R
+            assert _trunc_karatsuba_high(T, q, N, L) == (q * N) // R
+    assert crafted > 0
+    # the family really needs both corrections
+    N = next(n for n in (RNG.getrandbits(bits) | 1 | (1 << (bits - 1)) for _ in range(100))
+             if (n % X) % 2 and abs(n % X - n // X) % 2)
+    T = t_kara_trunc(RNG, N, L, 0, 0)
+    q = ((T % R) * ((-pow(N, -1, R)) % R)) % R
+    q0, q1, n0, n1 = q % X, q // X, N % X, N // X
+    assert _trunc_high_radix(q0, n0, H, 32, T % X) != _trunc_high_radix_no_corr(q0, n0, H, 32)
+    assert (q0 * n0) // X == _trunc_high_radix(q0, n0, H, 32, T % X)
+    dq, dnn = abs(q0 - q1), abs(n0 - n1)
+    assert (dq * dnn) // X != _trunc_high_radix_no_corr(dq, dnn, H, 32)
+
+
 # --------------------------------------------------------------------- modexp
 def test_modexp_exhaustive_tiny():
     for N in range(3, 1 << 6, 2):
