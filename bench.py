@@ -248,8 +248,13 @@ def run_ours(args) -> None:
     from paper_2410_18129_b200.launcher import Ranks
 
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    # MPB_BENCH_SHARE_GPU=1 (launcher check only, never a scaling number): every rank on device 0,
+    # gloo for the barrier and the reductions -- exercises the multi-rank path on a one-GPU box
+    share = os.environ.get("MPB_BENCH_SHARE_GPU") == "1"
+    if share:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
-    rk = Ranks("nccl", device=torch.device("cuda", local_rank))
+    rk = Ranks("gloo" if share else "nccl", device=torch.device("cuda", local_rank))
     rank, world = rk.rank, rk.world
     if world != args.gpus:
         raise SystemExit(f"bench.py: {world} rank(s) running but --gpus {args.gpus}")
@@ -402,6 +407,9 @@ def run_ours(args) -> None:
             "kernel_ms": {"mean": kern_ms, "min": float(np.min(per_launch_ms)), "max": float(np.max(per_launch_ms))},
             **extra,
         }
+        if share:
+            line["shared_gpu"] = ("MPB_BENCH_SHARE_GPU=1: all ranks on device 0 with gloo -- a check of the "
+                                  "multi-rank launcher and slicing, NOT a multi-GPU measurement")
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_oracle_sample()
         print(json.dumps(line), flush=True)
@@ -435,7 +443,7 @@ def main():
         from paper_2410_18129_b200.launcher import spawn
 
         have = torch.cuda.device_count()
-        if have < args.gpus:
+        if have < args.gpus and os.environ.get("MPB_BENCH_SHARE_GPU") != "1":
             raise SystemExit(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible")
         spawn(args.gpus, _rank_main, args)
         return
