@@ -15,6 +15,65 @@
 
 namespace mpb {
 
+#ifndef MPB_SCAN_U
+#define MPB_SCAN_U 1  // entries per step
+#endif
+#ifndef MPB_SCAN_G
+#define MPB_SCAN_G 8  // chunks (uint4) per group
+#endif
+#ifndef MPB_SCAN_LD
+#define MPB_SCAN_LD 0  // 0 evict-first (__ldcs), 1 default caching (__ldg)
+#endif
+
+// The CT masked full-table scan of a warp-tiled table of nent entries x Q4 chunks into a
+// per-thread shared-memory slot (word q at slot[q * blockDim]): every entry is read in full with a
+// mask, no address or branch depends on idx.  U entries x GR chunks in flight per step.
+template <int Q4, int U = MPB_SCAN_U, int GR = (MPB_SCAN_G < Q4 ? MPB_SCAN_G : Q4)>
+MPB_DEVI void scan_to_slot(const ArrT& G, int nent, uint32_t idx, uint32_t* slot) {
+    static_assert(Q4 % GR == 0, "whole chunk groups");
+#pragma unroll 1
+    for (int g0 = 0; g0 < Q4; g0 += GR) {
+        uint4 acc[GR];
+#pragma unroll
+        for (int q = 0; q < GR; q++) acc[q] = make_uint4(0, 0, 0, 0);
+#pragma unroll 1
+        for (int e0 = 0; e0 < nent; e0 += U) {
+            uint4 v[U][GR];
+#pragma unroll
+            for (int u = 0; u < U; u++)
+#pragma unroll
+                for (int q = 0; q < GR; q++) {
+                    const int c = (e0 + u) * Q4 + g0 + q;
+#if MPB_SCAN_LD == 1
+                    v[u][q] = e0 + u < nent ? __ldg(G.addr(c)) : make_uint4(0, 0, 0, 0);
+#else
+                    v[u][q] = e0 + u < nent ? G.ld_stream(c) : make_uint4(0, 0, 0, 0);
+#endif
+                }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const uint32_t x = (uint32_t)(e0 + u) ^ idx;
+                const uint32_t m = 0u - ((x - 1u) >> 31);  // all ones iff e == idx
+#pragma unroll
+                for (int q = 0; q < GR; q++) {
+                    acc[q].x |= v[u][q].x & m;
+                    acc[q].y |= v[u][q].y & m;
+                    acc[q].z |= v[u][q].z & m;
+                    acc[q].w |= v[u][q].w & m;
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < GR; q++) {
+            const int w0 = 4 * (g0 + q);
+            slot[(w0) * kThreads] = acc[q].x;
+            slot[(w0 + 1) * kThreads] = acc[q].y;
+            slot[(w0 + 2) * kThreads] = acc[q].z;
+            slot[(w0 + 3) * kThreads] = acc[q].w;
+        }
+    }
+}
+
 template <int L>
 __global__ void __launch_bounds__(kThreads, MPB_REG_MINB) k_modexp_reg(
     const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP, const uint32_t* __restrict__ R2,
@@ -54,32 +113,7 @@ __global__ void __launch_bounds__(kThreads, MPB_REG_MINB) k_modexp_reg(
         return v & ((1u << w) - 1u);
     };
     // CT masked full-table scan into the a slot
-    auto select = [&](uint32_t idx) {
-        uint4 acc[Q4];
-#pragma unroll
-        for (int q = 0; q < Q4; q++) acc[q] = make_uint4(0, 0, 0, 0);
-#pragma unroll 1
-        for (int e = 0; e < nent; e++) {
-            const uint32_t x = (uint32_t)e ^ idx;
-            const uint32_t m = 0u - ((x - 1u) >> 31);  // all ones iff e == idx
-            const ArrT Ge = G.at(e * Q4);
-#pragma unroll
-            for (int q = 0; q < Q4; q++) {
-                const uint4 v = Ge.ld_stream(q);
-                acc[q].x |= v.x & m;
-                acc[q].y |= v.y & m;
-                acc[q].z |= v.z & m;
-                acc[q].w |= v.w & m;
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < Q4; q++) {
-            sa[(4 * q) * kThreads] = acc[q].x;
-            sa[(4 * q + 1) * kThreads] = acc[q].y;
-            sa[(4 * q + 2) * kThreads] = acc[q].z;
-            sa[(4 * q + 3) * kThreads] = acc[q].w;
-        }
-    };
+    auto select = [&](uint32_t idx) { scan_to_slot<Q4>(G, nent, idx, sa); };
     // Flat schedule (public): op 0 G[0] = MontMul(R2, 1) (Montgomery one), op 1 G[1] = MontMul(base, R2),
     // op e < 2^w G[e] = MontMul(G[e-1], G[1]); then Y = G[top window]; per window w squarings, select,
     // one multiplication; last op out = MontMul(Y, 1).
@@ -206,32 +240,7 @@ __global__ void __launch_bounds__(kThreads, MPB_REG_MINB) k_modexp_rtr(
         if (off + w > 32 && wi + 1 < L) v |= word_at(exp, count, k, wi + 1) << (32 - off);
         return v & ((1u << w) - 1u);
     };
-    auto select = [&](uint32_t idx) {  // CT masked full-table scan into the a slot
-        uint4 acc[Q4];
-#pragma unroll
-        for (int q = 0; q < Q4; q++) acc[q] = make_uint4(0, 0, 0, 0);
-#pragma unroll 1
-        for (int e = 0; e < nent; e++) {
-            const uint32_t x = (uint32_t)e ^ idx;
-            const uint32_t m = 0u - ((x - 1u) >> 31);
-            const ArrT Ge = G.at(e * Q4);
-#pragma unroll
-            for (int q = 0; q < Q4; q++) {
-                const uint4 v = Ge.ld_stream(q);
-                acc[q].x |= v.x & m;
-                acc[q].y |= v.y & m;
-                acc[q].z |= v.z & m;
-                acc[q].w |= v.w & m;
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < Q4; q++) {
-            sa[(4 * q) * kThreads] = acc[q].x;
-            sa[(4 * q + 1) * kThreads] = acc[q].y;
-            sa[(4 * q + 2) * kThreads] = acc[q].z;
-            sa[(4 * q + 3) * kThreads] = acc[q].w;
-        }
-    };
+    auto select = [&](uint32_t idx) { scan_to_slot<Q4>(G, nent, idx, sa); };  // CT masked scan
     uint32_t y[L];
 #pragma unroll
     for (int q = 0; q < L; q++) y[q] = 0;
