@@ -553,9 +553,15 @@ __global__ void __launch_bounds__(kThreads) k_crt_recombine(const uint32_t* __re
 }
 
 // ---------------------------------------------------------------- launchers
+// stage buffers above the 48 KB default need the per-kernel opt-in (only with MPB_THREADS > 128 builds)
+template <class K>
+inline void smem_optin(K* k, size_t sm) {
+    if (sm > 48 * 1024) cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+}
 template <int C>
 void Launch<C>::setup(const uint32_t* N, uint32_t* NP, uint32_t* R2, size_t count, int nb, int pub_bits,
                       uint32_t* ws, cudaStream_t s) {
+    smem_optin(k_setup<C>, stage_bytes<C>());
     k_setup<C><<<(unsigned)((count + kThreads - 1) / kThreads), kThreads, stage_bytes<C>(), s>>>(N, NP, R2, count, nb,
                                                                                                pub_bits, ws);
 }
@@ -714,12 +720,15 @@ void Launch<C>::modexp(const uint32_t* N, const uint32_t* NP, const uint32_t* R2
             }
             auto go = [&](auto KL) {
                 constexpr int KLEV = decltype(KL)::value;
-                if (redc == 1)
+                if (redc == 1) {
+                    smem_optin(k_modexp<C, 1, NBT, KLEV>, sm);
                     k_modexp<C, 1, NBT, KLEV><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, k0, n, nb,
                                                                      bits, window, ws);
-                else
+                } else {
+                    smem_optin(k_modexp<C, 0, NBT, KLEV>, sm);
                     k_modexp<C, 0, NBT, KLEV><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, k0, n, nb,
                                                                      bits, window, ws);
+                }
             };
             // Karatsuba product phases are compiled for the large shapes only (f1); elsewhere schoolbook
             if constexpr (NBT == 0 || NBT == 8 || NBT == 11) {

@@ -1,8 +1,12 @@
 #!/bin/bash
-# CT scan variants of the 1024-bit register CIOS (tools/build_variant.py scan_*)
+# 2048-bit tail experiments at 2^18: 224-thread CTAs x 2; cooperative 2/4-lane tail
 mkdir -p gpurun_out
 for r in 1 2; do
-for lib in paper_2410_18129_b200/libmpb.so tune/libmpb_scan_u2.so tune/libmpb_scan_u4g4.so tune/libmpb_scan_ldg.so tune/libmpb_scan_u2ldg.so tune/libmpb_scan_u4g4ldg.so; do
-echo "$lib" >> gpurun_out/z_bench.log
-MPB_LIB=$lib python tools/bench_algo.py --bits 1024 --count 1048576 --algos 0 --redc 2 >> gpurun_out/z_bench.log 2>&1
+echo "base" >> gpurun_out/z_bench.log
+python tools/bench_algo.py --bits 2048 --count 262144 --algos 0 --redc 1 >> gpurun_out/z_bench.log 2>&1
+echo "t224" >> gpurun_out/z_bench.log
+MPB_LIB=tune/libmpb_t224.so python tools/bench_algo.py --bits 2048 --count 262144 --algos 0 --redc 1 >> gpurun_out/z_bench.log 2>&1
+for tl in 2 4; do
+echo "tail$tl" >> gpurun_out/z_bench.log
+MPB_COOP_TAIL=$tl python tools/bench_algo.py --bits 2048 --count 262144 --algos 0 --redc 1 >> gpurun_out/z_bench.log 2>&1
 done; done
