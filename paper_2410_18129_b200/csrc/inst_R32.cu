@@ -78,7 +78,7 @@ template <int L>
 __global__ void __launch_bounds__(kThreads, MPB_REG_MINB) k_modexp_reg(
     const uint32_t* __restrict__ N, const uint32_t* __restrict__ NP, const uint32_t* __restrict__ R2,
     const uint32_t* __restrict__ base, const uint32_t* __restrict__ exp, uint32_t* __restrict__ out, size_t count,
-    int bits, int w, uint32_t* ws) {
+    int bits, int w, uint32_t* ws, int sqr_rows) {
     const size_t k = tid_global();
     if (k >= count) return;
     constexpr int Q4 = L / 4;
@@ -124,9 +124,10 @@ __global__ void __launch_bounds__(kThreads, MPB_REG_MINB) k_modexp_reg(
     const int n_ops = nent + (nwin - 1) * per_win + 1;
 #pragma unroll 1
     for (int op = 0; op < n_ops; op++) {
-        uint32_t b[L];
+        uint32_t b[L + 1];  // the multiplicand (words 0 .. L-1) or, for a squaring, D = 2Y (L+1 words)
+        uint32_t(&bl)[L] = *reinterpret_cast<uint32_t(*)[L]>(b);
         int store_e = -1;
-        bool b_one = false, b_y = true;
+        bool b_one = false, b_y = true, sqr = false;
         if (op < nent) {
             store_e = op;
             if (op == 0) {
@@ -134,11 +135,11 @@ __global__ void __launch_bounds__(kThreads, MPB_REG_MINB) k_modexp_reg(
                 b_one = true;
             } else if (op == 1) {
                 a_from_mem(Bn);
-                ldb<L>(R2n, 0, b);
+                ldb<L>(R2n, 0, bl);
                 b_y = false;
             } else {
                 a_from_mem(G.at((op - 1) * Q4));
-                ldb<L>(G.at(Q4), 0, b);
+                ldb<L>(G.at(Q4), 0, bl);
                 b_y = false;
             }
         } else if (op == n_ops - 1) {
@@ -146,17 +147,24 @@ __global__ void __launch_bounds__(kThreads, MPB_REG_MINB) k_modexp_reg(
             b_one = true;
         } else {
             const int r = (op - nent) % per_win, win = nwin - 2 - (op - nent) / per_win;
-            if (r < w) a_from_regs(y);  // squaring: a = b = Y
-            else select(window(win));   // multiplication by the selected entry
+            if (r < w) {  // squaring: a = Y, squaring rows over B = 2Y
+                a_from_regs(y);
+                sqr = sqr_rows != 0;
+            } else {
+                select(window(win));  // multiplication by the selected entry
+            }
         }
         if (b_one) {
 #pragma unroll
             for (int q = 0; q < L; q++) b[q] = q == 0 ? 1u : 0u;
+        } else if (sqr) {
+            reg::double_words<L>(y, b);
         } else if (b_y) {
 #pragma unroll
             for (int q = 0; q < L; q++) b[q] = y[q];
         }
-        reg::montmul<L>(aw, b, n, n0p, y);
+        if (sqr) reg::montsqr<L>(aw, b, n, n0p, y);  // two call sites: MontSqr rows and MontMul rows
+        else reg::montmul<L>(aw, bl, n, n0p, y);
         if (store_e >= 0) stb<L>(G.at(store_e * Q4), 0, y);
         if (op == nent - 1) {  // after the table: Y = G[top window]
             select(window(nwin - 1));
@@ -172,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, MPB_REG_MINB) k_modexp_reg(
 template <int L>
 __global__ void __launch_bounds__(kThreads, MPB_REG_MINB) k_mont_mul_reg(
     const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, const uint32_t* __restrict__ N,
-    const uint32_t* __restrict__ NP, uint32_t* __restrict__ c, size_t count) {
+    const uint32_t* __restrict__ NP, uint32_t* __restrict__ c, size_t count, bool sqr) {
     const size_t k = tid_global();
     if (k >= count) return;
     extern __shared__ __align__(16) uint32_t smem_a[];
@@ -186,11 +194,17 @@ __global__ void __launch_bounds__(kThreads, MPB_REG_MINB) k_mont_mul_reg(
         sa[(4 * q + 2) * kThreads] = v.z;
         sa[(4 * q + 3) * kThreads] = v.w;
     }
-    uint32_t bb[L], n[L], y[L];
-    ldb<L>(arr(b, count, k), 0, bb);
+    uint32_t bb[L + 1], n[L], y[L];
+    ldb<L>(arr(sqr ? a : b, count, k), 0, y);
     ldb<L>(arr(N, count, k), 0, n);
     const uint32_t n0p = word_at(NP, count, k, 0);
-    reg::montmul<L>([&](int i) { return sa[i * kThreads]; }, bb, n, n0p, y);
+    auto aw = [&](int i) { return sa[i * kThreads]; };
+    if (sqr) {
+        reg::double_words<L>(y, bb);
+        reg::montsqr<L>(aw, bb, n, n0p, y);
+    } else {
+        reg::montmul<L>(aw, y, n, n0p, y);
+    }
     stb<L>(arr(c, count, k), 0, y);
 }
 
@@ -306,11 +320,21 @@ bool launch_modexp_rtr(const uint32_t* N, const uint32_t* NP, const uint32_t* R2
     return true;
 }
 
+// MPB_REG_SQR=0 runs MontSqr through the multiplication rows (A/B); default: squaring rows
+static int reg_sqr_rows() {
+    static int v = [] {
+        const char* e = getenv("MPB_REG_SQR");
+        return e ? atoi(e) : 1;
+    }();
+    return v;
+}
+
 bool launch_mont_mul_reg(const uint32_t* a, const uint32_t* b, const uint32_t* N, const uint32_t* NP, uint32_t* c,
                          size_t count, int bits, cudaStream_t s) {
     if (4 * ((bits + 127) / 128) != 32) return false;
     const unsigned g = (unsigned)((count + kThreads - 1) / kThreads);
-    k_mont_mul_reg<32><<<g, kThreads, (size_t)kThreads * 32 * 4, s>>>(a, b, N, NP, c, count);
+    k_mont_mul_reg<32><<<g, kThreads, (size_t)kThreads * 32 * 4, s>>>(a, b, N, NP, c, count,
+                                                                    a == b && reg_sqr_rows());
     return true;
 }
 
@@ -320,7 +344,7 @@ bool launch_modexp_reg(const uint32_t* N, const uint32_t* NP, const uint32_t* R2
     if (4 * ((bits + 127) / 128) != 32) return false;
     const unsigned g = (unsigned)((count + kThreads - 1) / kThreads);
     k_modexp_reg<32><<<g, kThreads, (size_t)kThreads * 32 * 4, s>>>(N, NP, R2, base, exp, out, count, bits, window,
-                                                                  ws);
+                                                                  ws, reg_sqr_rows());
     return true;
 }
 

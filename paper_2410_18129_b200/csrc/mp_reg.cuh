@@ -64,6 +64,35 @@ MPB_DEVI void row(uint32_t (&U)[2 * L + 2], uint32_t (&V)[2 * L + 2], uint32_t x
     }
 }
 
+// Y = positions L .. 2L of the finished rows (U[L + k] + V[L + k - 1] + cin, L + 1 words, < 2N),
+// then one masked subtraction of N: the canonical result.
+template <int L>
+MPB_DEVI void finish(const uint32_t (&U)[2 * L + 2], const uint32_t (&V)[2 * L + 2], uint32_t cin, const uint32_t (&N)[L],
+                     uint32_t (&out)[L]) {
+    uint32_t y[L + 1];
+#pragma unroll
+    for (int k = 0; k <= L; k++) y[k] = U[L + k];
+    add_first(y[0], cin);
+#pragma unroll
+    for (int k = 1; k <= L; k++) add_next(y[k], 0u);
+    add_first(y[0], V[L - 1]);
+#pragma unroll
+    for (int k = 1; k < L; k++) add_next(y[k], V[L + k - 1]);
+    add_end(y[L], V[2 * L - 1]);
+    // canonical: y >= N ? y - N : y (mask)
+    uint32_t d[L];
+#pragma unroll
+    for (int k = 0; k < L; k++) d[k] = y[k];
+    sub_first(d[0], N[0]);
+#pragma unroll
+    for (int k = 1; k < L; k++) sub_next(d[k], N[k]);
+    uint32_t top = y[L];
+    asm volatile("subc.u32 %0, %0, 0;" : "+r"(top));  // y[L] - borrow: 0 (y >= N) or -1 (y < N)
+    const uint32_t m = 0u - (top == 0u ? 1u : 0u);      // all ones: take y - N
+#pragma unroll
+    for (int k = 0; k < L; k++) out[k] = (d[k] & m) | (y[k] & ~m);
+}
+
 // OUT = a * b * 2^(-32L) mod N, canonical, for a, b < N.  a_i comes from `aw(i)` (a functor: the
 // caller streams it from shared memory); b, N in registers; n0p = -N^-1 mod 2^32.
 template <int L, int I, class AW>
@@ -94,29 +123,74 @@ MPB_DEVI void montmul(const AW& aw, const uint32_t (&b)[L], const uint32_t (&N)[
     for (int k = 0; k < 2 * L + 2; k++) { U[k] = 0; V[k] = 0; }
     uint32_t cin = 0;
     rows<L, 0>(U, V, cin, aw, b, N, n0p);
-    // Y = positions L .. 2L: U[L + k] + V[L + k - 1] + carries, L + 1 words (< 2N)
-    uint32_t y[L + 1];
+    finish<L>(U, V, cin, N, out);
+}
+
+// ---------------------------------------------------------------------------------------------------
+// MontSqr with SQUARING ROWS in the same CIOS order.  a^2 = sum_i a_i M_i 2^(32i) with
+// M_i = a_i + 2 sum_{j>i} a_j 2^(32(j-i)) (the textbook symmetric square: each cross product once,
+// doubled), so row i is a_i times the words j = i .. L of
+//     M[i] = a_i,  M[i+1] = D[i+1] with bit 0 cleared,  M[j] = D[j] (j > i+1),   D = 2a (L+1 words)
+// at positions i + j >= 2i.  Row i never reaches below position 2i >= i, so word i is complete when
+// m_i is formed, exactly as in CIOS; the reduction rows are montmul's.  L(L+1)/2 + L a-products
+// instead of L^2 (560 + 1024 reduction products instead of 2048 at L = 32).  Bounds: rows r <= i
+// sum to < 2a 2^(32(i+1)) <= 2^(32(i+L+1)+1) and the reductions to < N 2^(32i), so no chain carries
+// past position i+L+1, the top of the window (as in montmul).
+template <int L, int I>
+MPB_DEVI void row_sq(uint32_t (&U)[2 * L + 2], uint32_t (&V)[2 * L + 2], uint32_t x, const uint32_t (&D)[L + 1]) {
+    {  // U chain: j = I, I+2, .. <= L (positions 2I, 2I+2, ..)
+        constexpr int jl = L - ((L - I) & 1);
 #pragma unroll
-    for (int k = 0; k <= L; k++) y[k] = U[L + k];
-    add_first(y[0], cin);
+        for (int j = I; j <= L; j += 2)
+            pr_chain_rt(j == I, j == jl && jl == L, U[I + j], U[I + j + 1], x, j == I ? x : D[j]);
+        if constexpr (jl < L) absorb(U[I + L + 1]);
+    }
+    {  // V chain: j = I+1, I+3, .. <= L (positions 2I+1, ..; V index = position - 1)
+        constexpr int jl = L - ((L - I - 1) & 1);
 #pragma unroll
-    for (int k = 1; k <= L; k++) add_next(y[k], 0u);
-    add_first(y[0], V[L - 1]);
+        for (int j = I + 1; j <= L; j += 2)
+            pr_chain_rt(j == I + 1, j == jl && jl == L, V[I + j - 1], V[I + j], x, j == I + 1 ? (D[j] & ~1u) : D[j]);
+        if constexpr (jl < L) absorb(V[I + L]);
+    }
+}
+
+template <int L, int I, class AW>
+MPB_DEVI void rows_sq(uint32_t (&U)[2 * L + 2], uint32_t (&V)[2 * L + 2], uint32_t& cin, const AW& aw,
+                      const uint32_t (&D)[L + 1], const uint32_t (&N)[L], uint32_t n0p) {
+    if constexpr (I < L) {
+        row_sq<L, I>(U, V, aw(I), D);
+        uint32_t w = U[I] + cin;
+        if constexpr (I >= 1) w += V[I - 1];
+        const uint32_t m = w * n0p;
+        row<L, I>(U, V, m, N);
+        uint32_t lo = U[I], c = 0;
+        asm volatile("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, 0, 0;" : "+r"(lo), "+r"(c) : "r"(cin));
+        if constexpr (I >= 1) {
+            asm volatile("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, 0;" : "+r"(lo), "+r"(c) : "r"(V[I - 1]));
+        }
+        cin = c;
+        rows_sq<L, I + 1>(U, V, cin, aw, D, N, n0p);
+    }
+}
+
+// out = a^2 * 2^(-32L) mod N canonical, a < N: aw(i) = a_i, D = 2a (double_words)
+template <int L, class AW>
+MPB_DEVI void montsqr(const AW& aw, const uint32_t (&D)[L + 1], const uint32_t (&N)[L], uint32_t n0p, uint32_t (&out)[L]) {
+    uint32_t U[2 * L + 2], V[2 * L + 2];
 #pragma unroll
-    for (int k = 1; k < L; k++) add_next(y[k], V[L + k - 1]);
-    add_end(y[L], V[2 * L - 1]);
-    // canonical: y >= N ? y - N : y (mask)
-    uint32_t d[L];
+    for (int k = 0; k < 2 * L + 2; k++) { U[k] = 0; V[k] = 0; }
+    uint32_t cin = 0;
+    rows_sq<L, 0>(U, V, cin, aw, D, N, n0p);
+    finish<L>(U, V, cin, N, out);
+}
+
+// B = 2a as L+1 words (the squaring rows' multiplicand)
+template <int L>
+MPB_DEVI void double_words(const uint32_t (&a)[L], uint32_t (&B)[L + 1]) {
+    B[0] = a[0] << 1;
 #pragma unroll
-    for (int k = 0; k < L; k++) d[k] = y[k];
-    sub_first(d[0], N[0]);
-#pragma unroll
-    for (int k = 1; k < L; k++) sub_next(d[k], N[k]);
-    uint32_t top = y[L];
-    asm volatile("subc.u32 %0, %0, 0;" : "+r"(top));  // y[L] - borrow: 0 (y >= N) or -1 (y < N)
-    const uint32_t m = 0u - (top == 0u ? 1u : 0u);      // all ones: take y - N
-#pragma unroll
-    for (int k = 0; k < L; k++) out[k] = (d[k] & m) | (y[k] & ~m);
+    for (int q = 1; q < L; q++) B[q] = __funnelshift_l(a[q - 1], a[q], 1);
+    B[L] = a[L - 1] >> 31;
 }
 
 }  // namespace reg

@@ -126,6 +126,51 @@ def test_mont_mul_sqr(mpb, bits, redc):
     assert np.array_equal(s, ref_s)
 
 
+def test_mont_sqr_rows_register(mpb):
+    """The register CIOS MontSqr's squaring rows at 1024 bits (mp_reg.cuh montsqr: row i = a_i times
+    a_i, 2a's word i+1 with bit 0 cleared, 2a's words above; D = 2a has L+1 words).  Operands whose
+    words all have the top bit set (every D word carries a bit in from below, so the bit-0 clearing
+    of M[i+1] matters in every row), all-ones moduli (N = 2^1024 - small, a = N - 1: D[L] = 1 and the
+    largest carries), alternating patterns, powers of two, against the oracle."""
+    bits, count = 1024, 96
+    L = I.limbs_for_bits(bits)
+    N, a, _, dN, Np, R2 = _mont_fixture(mpb, bits, count, config=1)
+    rng = np.random.default_rng(77)
+    M = (1 << 32) - 1
+    Ns = ints(N)
+    for k in range(count):
+        n = Ns[k]
+        kind = k % 8
+        if kind == 0:  # every word's top bit set, a < N
+            v = int.from_bytes(rng.bytes(L * 4), "little") | int("80000000" * L, 16)
+            v %= n
+        elif kind == 1:  # N = 2^1024 - odd small, a = N - 1
+            n = (1 << bits) - (2 * int(rng.integers(1, 1 << 20)) + 1)
+            v = n - 1
+        elif kind == 2:  # alternating words, top bits set
+            v = int(("AAAAAAAA" + "D5555555") * (L // 2), 16) % n
+        elif kind == 3:
+            v = 1 << int(rng.integers(0, bits - 1))
+            v %= n
+        elif kind == 4:
+            v = n - 1
+        elif kind == 5:  # words 0xFFFFFFFF except one
+            v = ((1 << bits) - 1 - (M << (32 * int(rng.integers(0, L))))) % n
+        else:
+            v = int.from_bytes(rng.bytes(L * 4), "little") % n
+        N[k] = I.to_limbs(n, L)
+        a[k] = I.to_limbs(v, L)
+    dN = mpb.to_device(N)
+    Np, R2 = mpb.mont_batch_setup(dN, bits)
+    s = mpb.to_host(mpb.mont_batch_sqr(mpb.to_device(a), dN, Np, bits, redc=mpb.REDC_CIOS))
+    assert np.array_equal(s, O.batch_montmul(a, a, N))
+    # the same operands through the exponentiation (squarings dominate: w squaring rows per window)
+    e = np.full((count, L), M, dtype=np.uint32)
+    out = mpb.to_host(mpb.mont_batch_modexp_ct(dN, Np, R2, mpb.to_device(a), mpb.to_device(e), bits, window=5,
+                                               redc=mpb.REDC_CIOS))
+    assert np.array_equal(out, O.batch_modexp(a, e, bits, N))
+
+
 # --------------------------------------------------------------------- REDC
 @pytest.mark.parametrize("redc", REDC_STANDALONE)
 @pytest.mark.parametrize("bits", BITS_MOD + BITS_ODD)

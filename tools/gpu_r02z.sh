@@ -1,12 +1,9 @@
 #!/bin/bash
-# 2048-bit tail experiments at 2^18: 224-thread CTAs x 2; cooperative 2/4-lane tail
+# squaring rows: focused tests, config 1/2 suite lines, one ncu --set full of the 1024-bit CIOS launch
 mkdir -p gpurun_out
-for r in 1 2; do
-echo "base" >> gpurun_out/z_bench.log
-python tools/bench_algo.py --bits 2048 --count 262144 --algos 0 --redc 1 >> gpurun_out/z_bench.log 2>&1
-echo "t224" >> gpurun_out/z_bench.log
-MPB_LIB=tune/libmpb_t224.so python tools/bench_algo.py --bits 2048 --count 262144 --algos 0 --redc 1 >> gpurun_out/z_bench.log 2>&1
-for tl in 2 4; do
-echo "tail$tl" >> gpurun_out/z_bench.log
-MPB_COOP_TAIL=$tl python tools/bench_algo.py --bits 2048 --count 262144 --algos 0 --redc 1 >> gpurun_out/z_bench.log 2>&1
-done; done
+timeout 600 python -m pytest tests -m gpu -x -q -k "sqr_rows or cios_register or mont_mul_sqr or crt" > gpurun_out/z_tests.log 2>&1
+echo "tests rc=$?" >> gpurun_out/z_tests.log
+python tools/bench_suite.py --configs 1,2 > gpurun_out/z_suite12.jsonl 2>&1
+P="python tools/prof_modexp.py --bits 1024 --count 56832 --redc 2"
+$P > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_modexp -c 1 -f -o gpurun_out/z_cios_sqr $P > gpurun_out/z_ncu.log 2>&1
+echo done
