@@ -58,13 +58,14 @@ def imad_counts(L: int, redc: int) -> dict:
     redc: 1 truncated, 0 full, 2 CIOS (alg:8BlockMontRed at digit 2^(32C): per row of C limbs,
     2CL products for a_i*B, 2CL for m_i*N and a C x C low-half product of C^2 IMAD, so
     4L^2 + LC for a multiplication or a squaring; REDC is MontMul(X, 1).  At L = 32 the
-    register-resident kernel (csrc/mp_reg.cuh) uses the paper's word digit: C = 1, 4L^2 + L, and
-    squares with symmetric squaring rows: 2(L(L+1)/2 + L) + 2L^2 + L = 3L^2 + 4L)."""
+    register-resident kernel (csrc/mp_reg.cuh) uses the paper's word digit: C = 1, 4L^2 + L.
+    MontSqr uses squaring rows (each cross product once, doubled): at block granularity
+    NB(NB-1)/2 full blocks + NB symmetric C x C squares = L^2 + L for the a-part, so 3L^2 + L + LC;
+    the register kernel's word rows also multiply by the top word of 2a: 3L^2 + 4L)."""
     if redc == 2:
         C = 1 if L == 32 else block_for(L)  # 1024 bits: the register-resident kernel's 32-bit digit
-        mul = sqr = redc_ = 4 * L * L + L * C
-        if L == 32:
-            sqr = 3 * L * L + 4 * L  # reg::montsqr (MPB_REG_SQR=0 would run 4L^2 + L)
+        mul = redc_ = 4 * L * L + L * C
+        sqr = 3 * L * L + 4 * L if L == 32 else 3 * L * L + L + L * C
     elif redc:
         mul, sqr, redc_ = 4 * L * L + 2 * L - 1, 3 * L * L + 3 * L - 1, 2 * L * L + 2 * L - 1
     else:

@@ -343,6 +343,9 @@ MPB_DEVI void mont_op_k(int mode, int NB, const AR& X, const AR& B, const AR& N,
     }
 }
 
+#ifndef MPB_CIOS_SQR
+#define MPB_CIOS_SQR 1  // 0: CIOS squares through the multiplication rows (A/B builds)
+#endif
 // Any REDC mode: RM = 0 full (alg:8MontRed), 1 truncated (alg:trunc_montred), 2 CIOS
 // (alg:8BlockMontRed, schoolbook only: the reduction is interleaved with the product rows).
 // CIOS uses T as its Y scratch and Q as its m scratch; REDC(X) is MontMul(X, 1).
@@ -351,7 +354,7 @@ MPB_DEVI void mont_op_rm(int mode, int NB, const AR& X, const AR& B, const AR& N
                          const AR& Q, const AR& OUT, const AR& KS, const Stage& sg) {
     if constexpr (RM == 2) {
         static_assert(KLEV == 0, "CIOS interleaves reduction and product rows: schoolbook only");
-        cios_op<C>(NB, X, B, mode == MODE_REDC, N, NP, T, Q, OUT);
+        cios_op<C>(NB, X, B, mode == MODE_REDC, N, NP, T, Q, OUT, mode == MODE_SQR && MPB_CIOS_SQR);
     } else {
         mont_op_k<C, RM == 1, KLEV>(mode, NB, X, B, N, NP, T, Q, OUT, KS, sg);
     }

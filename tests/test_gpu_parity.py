@@ -126,13 +126,16 @@ def test_mont_mul_sqr(mpb, bits, redc):
     assert np.array_equal(s, ref_s)
 
 
-def test_mont_sqr_rows_register(mpb):
-    """The register CIOS MontSqr's squaring rows at 1024 bits (mp_reg.cuh montsqr: row i = a_i times
-    a_i, 2a's word i+1 with bit 0 cleared, 2a's words above; D = 2a has L+1 words).  Operands whose
-    words all have the top bit set (every D word carries a bit in from below, so the bit-0 clearing
-    of M[i+1] matters in every row), all-ones moduli (N = 2^1024 - small, a = N - 1: D[L] = 1 and the
-    largest carries), alternating patterns, powers of two, against the oracle."""
-    bits, count = 1024, 96
+@pytest.mark.parametrize("bits", [1024, 2048, 3072, 4096])
+def test_mont_sqr_rows(mpb, bits):
+    """CIOS MontSqr by squaring rows.  1024 bits: the register kernel (mp_reg.cuh montsqr: row i =
+    a_i times a_i, 2a's word i+1 with bit 0 cleared, 2a's words above; D = 2a has L+1 words).  Larger
+    sizes: the block engine (mp_mont.cuh cios_op, sqr: a_i^2 at pass i, 2 a_i a_t above).  Operands
+    whose words all have the top bit set (every D word carries a bit in from below; every doubled
+    block product carries out of its top word), all-ones moduli (N = 2^bits - small, a = N - 1: the
+    largest carries, Y up to 3N between rows), alternating patterns, powers of two, against the
+    oracle."""
+    count = 96 if bits <= 2048 else 40
     L = I.limbs_for_bits(bits)
     N, a, _, dN, Np, R2 = _mont_fixture(mpb, bits, count, config=1)
     rng = np.random.default_rng(77)
@@ -144,7 +147,10 @@ def test_mont_sqr_rows_register(mpb):
         if kind == 0:  # every word's top bit set, a < N
             v = int.from_bytes(rng.bytes(L * 4), "little") | int("80000000" * L, 16)
             v %= n
-        elif kind == 1:  # N = 2^1024 - odd small, a = N - 1
+            v |= int("80000000" * (L - 1), 16) & ((1 << (32 * (L - 1))) - 1)  # keep the low words' top bits
+            if v >= n:
+                v %= n
+        elif kind == 1:  # N = 2^bits - odd small, a = N - 1
             n = (1 << bits) - (2 * int(rng.integers(1, 1 << 20)) + 1)
             v = n - 1
         elif kind == 2:  # alternating words, top bits set

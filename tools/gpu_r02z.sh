@@ -1,9 +1,12 @@
 #!/bin/bash
-# squaring rows: focused tests, config 1/2 suite lines, one ncu --set full of the 1024-bit CIOS launch
+# block-engine CIOS squaring rows: parity subset + A/B (tune/libmpb_csq0.so = multiplication rows)
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests -m gpu -x -q -k "sqr_rows or cios_register or mont_mul_sqr or crt" > gpurun_out/z_tests.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q -k "cios or mont_mul_sqr or modexp or crt" > gpurun_out/z_tests.log 2>&1
 echo "tests rc=$?" >> gpurun_out/z_tests.log
-python tools/bench_suite.py --configs 1,2 > gpurun_out/z_suite12.jsonl 2>&1
-P="python tools/prof_modexp.py --bits 1024 --count 56832 --redc 2"
-$P > /dev/null 2>&1 && ncu --set full --clock-control none --import-source on -k regex:k_modexp -c 1 -f -o gpurun_out/z_cios_sqr $P > gpurun_out/z_ncu.log 2>&1
-echo done
+for r in 1 2; do
+for lib in paper_2410_18129_b200/libmpb.so tune/libmpb_csq0.so; do
+echo "$lib" >> gpurun_out/z_bench.log
+MPB_LIB=$lib python tools/bench_algo.py --bits 2048 --count 262144 --algos 0 --redc 2 >> gpurun_out/z_bench.log 2>&1
+MPB_LIB=$lib python tools/bench_algo.py --bits 4096 --count 65536 --algos 0 --redc 2 >> gpurun_out/z_bench.log 2>&1
+MPB_LIB=$lib python tools/bench_algo.py --bits 3072 --count 131072 --algos 0 --redc 2 >> gpurun_out/z_bench.log 2>&1
+done; done
