@@ -22,6 +22,7 @@ ap.add_argument("--cls", choices=["zero", "ones", "random"], required=True)
 ap.add_argument("--count", type=int, default=148 * 128)
 ap.add_argument("--bits", type=int, default=2048)
 ap.add_argument("--algo", type=int, default=0)  # 4 = radix-2^52 kernel
+ap.add_argument("--redc", type=int, default=1)  # 2 = CIOS (1024 bits: the register kernel)
 a = ap.parse_args()
 N, base, exp = I.modexp_inputs(config=3, count=a.count, bits=a.bits)
 L = N.shape[1]
@@ -35,6 +36,6 @@ elif a.cls == "ones":
     exp[:, (a.bits + 31) // 32:] = 0
 dN, dB, dE = (mpb.to_device(x) for x in (N, base, exp))
 Np, R2 = mpb.mont_batch_setup(dN, a.bits)
-out = mpb.mont_batch_modexp_ct(dN, Np, R2, dB, dE, a.bits, 5, 1, algo=a.algo)
+out = mpb.mont_batch_modexp_ct(dN, Np, R2, dB, dE, a.bits, 5, a.redc, algo=a.algo)
 torch.cuda.synchronize()
 print("ok", a.cls, int(mpb.to_host(out)[0, 0]))
