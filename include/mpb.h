@@ -48,7 +48,8 @@ typedef enum { MPB_OK = 0, MPB_EINVAL = -1, MPB_EUNSUPPORTED = -2, MPB_ECUDA = -
  * to a stand-alone mont_batch_redc (MPB_EUNSUPPORTED).  At 1024 bits CIOS runs a register-resident
  * kernel with the paper's 32-bit word digit (n0' = Nprime limb 0).  MontSqr under CIOS uses squaring
  * rows (each cross product once, doubled, at word or block granularity); the result is the same
- * value a^2 R^-1 mod N.  mont_batch_mul with a == b (the same pointer) is a squaring. */
+ * value a^2 R^-1 mod N (at 1024 bits mont_batch_mul with a == b, the same pointer, also takes the
+ * squaring rows). */
 enum { MPB_REDC_FULL = 0, MPB_REDC_TRUNCATED = 1, MPB_REDC_CIOS = 2 };
 /* AUTO = schoolbook: on sm_100a the blocked schoolbook engine beat every Karatsuba variant at every
  * measured size, so there is no crossover to select; KARATSUBA = one level,
