@@ -149,6 +149,10 @@ __global__ void __launch_bounds__(kThreads) k_mont_redc(const uint32_t* __restri
     mont_op<C, TRUNC>(MODE_REDC, nb, T, T, arr(N, count, k), arr(NP, count, k), T, Q, arr(c, count, k), stage());
 }
 
+#ifndef MPB_TBL_PF
+#define MPB_TBL_PF 0  // L2 bulk prefetch of the window table this many squarings before its scan (0: off)
+#endif
+
 // warp-tiled view of operand k in an array of nch chunks per operand (DESIGN 5.6)
 MPB_DEVI ArrT tarr(uint32_t* base, int nch, size_t k) {
     char* p = reinterpret_cast<char*>(base) + (k >> 5) * ((size_t)nch * kTileSB) + (k & 31) * 16;
@@ -330,6 +334,29 @@ MPB_DEVI void modexp_body(const uint32_t* N, const uint32_t* NP, const uint32_t*
             }
             continue;
         }
+#if MPB_TBL_PF
+        // L2 bulk prefetch of this warp's window table (one contiguous region of the warp tile:
+        // nent * Q4 chunk rows x 512 bytes), issued MPB_TBL_PF squarings before the CT scan of a
+        // window so its HBM reads spread over compute-bound squarings instead of arriving in one
+        // burst.  Public addresses and a public schedule: always the whole table.
+        if constexpr (TILE && !COOP) {
+            if (op > nent && op < n_ops - 1 && (op - nent - 1) % per_win == w - MPB_TBL_PF) {
+                const uint32_t lane = threadIdx.x & 31u;
+                const char* tb = reinterpret_cast<const char*>(G.p) - lane * 16u;  // tile base
+                const uint32_t tbytes = (uint32_t)nent * (uint32_t)Q4 * kTileSB;
+#if MPB_TBL_PF_ONE  // one lane, one bulk prefetch of MPB_TBL_PF_ONE / 32 of the table
+                if (lane == 0)
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(tb),
+                                 "r"(tbytes / 32u * (uint32_t)MPB_TBL_PF_ONE)
+                                 : "memory");
+#else
+                const uint32_t piece = tbytes / 32u;  // multiple of 16: nent * Q4 * 16
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(tb + lane * piece), "r"(piece)
+                             : "memory");
+#endif
+            }
+        }
+#endif
         if (RM != 2 && mode == MODE_REDC) {  // T = X zero-extended to 2L limbs (CIOS: MontMul(X, 1))
             if (!COOP || role == 0) {  // one writer per operand
 #pragma unroll 1
