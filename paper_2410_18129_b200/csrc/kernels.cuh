@@ -149,6 +149,9 @@ __global__ void __launch_bounds__(kThreads) k_mont_redc(const uint32_t* __restri
     mont_op<C, TRUNC>(MODE_REDC, nb, T, T, arr(N, count, k), arr(NP, count, k), T, Q, arr(c, count, k), stage());
 }
 
+#ifndef MPB_LOCKSTEP
+#define MPB_LOCKSTEP 0
+#endif
 #ifndef MPB_TBL_PF
 #define MPB_TBL_PF 0  // L2 bulk prefetch of the window table this many squarings before its scan (0: off)
 #endif
@@ -296,6 +299,14 @@ MPB_DEVI void modexp_body(const uint32_t* N, const uint32_t* NP, const uint32_t*
     const int n_ops = nent + 1 + (nwin - 1) * per_win + 1;
 #pragma unroll 1
     for (int op = 0; op < n_ops; op++) {
+#if MPB_LOCKSTEP
+        // keep the CTA's warps in step (the warp scheduler favours some warps; a CTA whose warps
+        // drift apart ends at its slowest warp's time).  Public schedule: a barrier every
+        // MPB_LOCKSTEP operations.
+        if constexpr (!COOP) {
+            if (op % MPB_LOCKSTEP == 0) __syncthreads();
+        }
+#endif
         int mode = MODE_MUL;
         bool select = false;
         int win = 0;
@@ -386,6 +397,10 @@ MPB_DEVI void modexp_body(const uint32_t* N, const uint32_t* NP, const uint32_t*
     }
 }
 
+#ifdef MPB_CTA_TIMES
+static __device__ unsigned long long g_cta_t0[1 << 14], g_cta_t1[1 << 14];
+static __device__ uint32_t g_cta_sm[1 << 14];
+#endif
 // One thread per operand: operands k_ofs .. k_ofs + n_run - 1 of a batch of `count`.
 template <int C, int RM, int NBT, int KLEV, int MINB = min_blocks<C>()>
 __global__ void __launch_bounds__(kThreads, MINB) k_modexp(
@@ -393,9 +408,24 @@ __global__ void __launch_bounds__(kThreads, MINB) k_modexp(
     const uint32_t* __restrict__ base, const uint32_t* __restrict__ exp, uint32_t* __restrict__ out, size_t count,
     size_t k_ofs, size_t n_run, int nb_rt, int bits, int w, uint32_t* ws) {
     const size_t t = tid_global();
+#ifdef MPB_CTA_TIMES  // DIAGNOSTIC builds only (tools/cta_times.cu): per-CTA start / end / SM
+    if (threadIdx.x == 0) {
+        unsigned long long t0;
+        uint32_t sm;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        g_cta_t0[blockIdx.x] = t0;
+        g_cta_sm[blockIdx.x] = sm;
+    }
+#endif
     if (t >= n_run) return;
     modexp_body<C, RM, NBT, KLEV, 1>(N, NP, R2, base, exp, out, count, k_ofs + t, nb_rt, bits, w, ws, 0u,
                                      0xFFFFFFFFu);
+#ifdef MPB_CTA_TIMES
+    unsigned long long t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    atomicMax(&g_cta_t1[blockIdx.x], t1);
+#endif
 }
 
 // One thread per operand, operand blocks loaded as per-warp TMA tiles (engine<.., TMA = true>).
@@ -712,6 +742,14 @@ inline int tma_policy() {
     }();
     return v;
 }
+// MPB_ONEWAVE=0: no one-CTA-per-SM instances for one-wave batches (tests and A/B measurements)
+inline int onewave_policy() {
+    static int v = [] {
+        const char* e = getenv("MPB_ONEWAVE");
+        return e ? atoi(e) : 1;
+    }();
+    return v;
+}
 // MPB_COOP: unset = the measured policy; 0 = always one thread per operand; 1 or 2 / 4 / 8 =
 // always 2 / 2 / 4 / 8 lanes per operand (tests and tuning)
 inline int coop_policy() {
@@ -739,6 +777,27 @@ void Launch<C>::modexp(const uint32_t* N, const uint32_t* NP, const uint32_t* R2
         constexpr int NBT = decltype(NBc)::value;
         auto single = [&](size_t k0, size_t n) {
             if (n == 0) return;
+            if constexpr ((C == 16 && (NBT == 2 || NBT == 4 || NBT == 6 || NBT == 8)) || (C == 12 && NBT == 11)) {
+                // A batch that fits one wave: one CTA of <= 384 (<= 448 at 4096 bits) threads per SM,
+                // the batch spread evenly over the SMs (inst_W384.cu / inst_W448.cu).
+                // Measured: 2^16 x 4096 bits 49.4 K vs 46.1 K/s (4 x 128-thread CTAs per SM),
+                // 56 832 x 2048 bits 398 K vs 365 K/s (3 x 128).
+                if (levels == 0 && onewave_policy() != 0) {
+                    int dev = 0, sms = 148;
+                    if (cudaGetDevice(&dev) == cudaSuccess)
+                        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+                    const size_t per = (n + (size_t)sms - 1) / (size_t)sms;
+                    const unsigned thr = (unsigned)((per + 31) / 32 * 32);
+                    const unsigned gw = (unsigned)((n + thr - 1) / thr);
+                    if (thr <= 384 && ::mpb_modexp_w384(N, NP, R2, base, exp, out, count, k0, n, C, nb, bits,
+                                                        window, redc, ws, gw, thr, s))
+                        return;
+                    if ((NBT == 8 || NBT == 11) && thr <= 448 &&
+                        ::mpb_modexp_w448(N, NP, R2, base, exp, out, count, k0, n, C, nb, bits, window, redc, ws,
+                                          gw, thr, s))
+                        return;
+                }
+            }
             const unsigned g = grid_for(n);
             if (redc == 2) {  // CIOS: schoolbook rows only
                 k_modexp<C, 2, NBT, 0><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, k0, n, nb, bits,

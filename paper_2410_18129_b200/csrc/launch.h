@@ -81,3 +81,16 @@ inline int kara_scratch_blocks_host(int nb, int level) {
 inline int block_for(int L) { return L % 16 == 0 ? 16 : (L % 12 == 0 ? 12 : (L % 8 == 0 ? 8 : 4)); }
 
 }  // namespace mpb
+
+// One-wave exponentiation instances (inst_W384.cu, inst_W448.cu): the same
+// k_modexp code compiled for one CTA of up to 384 (168 registers) or 448 (128 registers) threads
+// per SM, launched as `grid` CTAs of `threads` (a multiple of 32) threads on stream s.  A batch
+// that fits one wave runs faster this way than as several 128-thread CTAs per SM, whose warps the
+// scheduler serves unevenly (the launch ends with its most starved CTA).  false: the block count
+// (C, nb) or redc is not compiled in that unit (the caller falls back).
+bool mpb_modexp_w384(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
+                     const uint32_t* exp, uint32_t* out, size_t count, size_t k0, size_t n, int C, int nb,
+                     int bits, int window, int redc, uint32_t* ws, unsigned grid, unsigned threads, cudaStream_t s);
+bool mpb_modexp_w448(const uint32_t* N, const uint32_t* NP, const uint32_t* R2, const uint32_t* base,
+                     const uint32_t* exp, uint32_t* out, size_t count, size_t k0, size_t n, int C, int nb,
+                     int bits, int window, int redc, uint32_t* ws, unsigned grid, unsigned threads, cudaStream_t s);

@@ -907,7 +907,7 @@ for bits, count, w, redc in ((1024, 9, 5, 1), (2048, 5, 4, 0), (3072, 4, 5, 1), 
 """
 
 
-@pytest.mark.parametrize("coop", ["0", "1", "4", "8", "tma"])
+@pytest.mark.parametrize("coop", ["0", "0-nowave", "1", "4", "8", "tma"])
 def test_modexp_one_thread_and_two_lane_kernels(mpb, coop):
     """All exponentiation kernels, forced by MPB_COOP / MPB_TMA in a subprocess (the policy is read
     once per process): one thread per operand (0), two / four / eight lanes per operand (1, 4, 8:
@@ -918,7 +918,12 @@ def test_modexp_one_thread_and_two_lane_kernels(mpb, coop):
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, MPB_COOP="0", MPB_TMA="1") if coop == "tma" else dict(os.environ, MPB_COOP=coop)
+    if coop == "tma":
+        env = dict(os.environ, MPB_COOP="0", MPB_TMA="1")
+    elif coop == "0-nowave":  # one thread per operand, 128-thread CTAs (no one-wave instances)
+        env = dict(os.environ, MPB_COOP="0", MPB_ONEWAVE="0")
+    else:
+        env = dict(os.environ, MPB_COOP=coop)
     res = subprocess.run([sys.executable, "-c", _COOP_SCRIPT % root], env=env, capture_output=True, text=True,
                          timeout=600)
     assert res.returncode == 0, res.stderr[-2000:]
@@ -931,6 +936,52 @@ def test_modexp_one_thread_and_two_lane_kernels(mpb, coop):
         got = np.frombuffer(bytes.fromhex(hx), dtype=np.uint32).reshape(count, L)
         N, base, exp = I.modexp_inputs(config=4, count=count, bits=bits)
         assert np.array_equal(got, O.batch_modexp(base, exp, bits, N)), (bits, coop)
+
+
+_ONEWAVE_SCRIPT = r"""
+import sys, hashlib, numpy as np
+sys.path.insert(0, %r)
+from paper_2410_18129_b200 import inputs as I, mpb
+for bits, count, redc in %r:
+    N, base, exp = I.modexp_inputs(config=4, count=count, bits=bits)
+    dN = mpb.to_device(N)
+    Np, R2 = mpb.mont_batch_setup(dN, bits)
+    o = mpb.to_host(mpb.mont_batch_modexp_ct(dN, Np, R2, mpb.to_device(base), mpb.to_device(exp), bits, window=5,
+                                             redc=redc))
+    print(bits, count, redc, hashlib.sha256(o.tobytes()).hexdigest())
+"""
+
+# (bits, count, redc): batches of one wave or less, so the one-CTA-per-SM instances run with
+# 64..448-thread CTAs and ragged last CTAs (count not a multiple of the CTA size)
+_ONEWAVE_CASES = ((1024, 10007, 1), (2048, 20011, 1), (2048, 4740, 0), (2048, 9000, 2), (3072, 30001, 1),
+                  (4096, 60001, 1), (4096, 12001, 0), (4108, 50001, 1), (4108, 65536, 0))
+
+
+def test_modexp_onewave_instances(mpb):
+    """One-wave batches run as one CTA of up to 384 / 448 threads per SM (inst_W384.cu / inst_W448.cu,
+    DESIGN.md 5.3c): every output equals the 128-thread kernels' (MPB_ONEWAVE=0, a subprocess: the
+    policy is read once per process) on the whole batch, and a sample including the first and last
+    operand equals the oracle."""
+    import hashlib
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, "-c", _ONEWAVE_SCRIPT % (root, _ONEWAVE_CASES)],
+                         env=dict(os.environ, MPB_ONEWAVE="0"), capture_output=True, text=True, timeout=900)
+    assert res.returncode == 0, res.stderr[-2000:]
+    ref = {tuple(map(int, l.split()[:3])): l.split()[3] for l in res.stdout.splitlines() if l.strip()}
+    assert len(ref) == len(_ONEWAVE_CASES)
+    for bits, count, redc in _ONEWAVE_CASES:
+        N, base, exp = I.modexp_inputs(config=4, count=count, bits=bits)
+        dN = mpb.to_device(N)
+        Np, R2 = mpb.mont_batch_setup(dN, bits)
+        out = mpb.to_host(mpb.mont_batch_modexp_ct(dN, Np, R2, mpb.to_device(base), mpb.to_device(exp), bits,
+                                                   window=5, redc=redc))
+        assert hashlib.sha256(out.tobytes()).hexdigest() == ref[(bits, count, redc)], (bits, count, redc)
+        idx = np.array(sorted({0, count - 1, *np.random.default_rng(count).choice(count, 3, replace=False)}))
+        assert np.array_equal(out[idx], O.batch_modexp(base[idx], exp[idx], bits, N[idx])), (bits, count, redc)
 
 
 # ----------------------------------------------------------------------- fuzz
