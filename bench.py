@@ -353,9 +353,44 @@ def run_ours(args) -> None:
                   "frac_modsqr": ms_ * c2["sqr"] / (SMS * IMAD_PER_CLK_SM * 1965e6)}
         del dN2, da2, db2, Np2, ws2, o2
 
+    # config 4 (4096-bit modexp, w = 5, truncated REDC, 2^16 operands: one wave, one 448-thread CTA
+    # per SM): mean CUDA-event time of 2 launches after one warm-up (not the headline's
+    # timed region)
+    config4 = None
+    if rank == 0 and not c5 and not args.no_config4:
+        b4, n4 = 4096, 1 << 16
+        N4, B4, E4 = I.modexp_inputs(config=4, count=n4, bits=b4)
+        dN4, dB4, dE4 = (mpb.to_device(x) for x in (N4, B4, E4))
+        Np4, R24 = mpb.mont_batch_setup(dN4, b4)
+        ws4 = mpb.modexp_workspace(n4, b4, WINDOW, 0)
+        o4 = mpb.empty_sliced(I.limbs_for_bits(b4), n4)
+
+        def run4():
+            mpb.mont_batch_modexp_ct(dN4, Np4, R24, dB4, dE4, b4, WINDOW, mpb.REDC_TRUNCATED, ws=ws4, out=o4)
+
+        run4()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(torch.cuda.current_stream())
+        for _ in range(2):
+            run4()
+        e1.record(torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        r4 = n4 * 2 / (e0.elapsed_time(e1) / 1000.0)
+        peak = SMS * IMAD_PER_CLK_SM * 1965e6
+        config4 = {"workload": "BASELINE config 4: 4096-bit CT modexp, w = 5, truncated REDC, 2^16 operands "
+                               "(register-Karatsuba blocks, one 448-thread CTA per SM)",
+                   "modexp_per_s": r4, "unit": "modexp/s",
+                   "frac_own_count": r4 * modexp_imad(b4, WINDOW, 1, own=True) / peak,
+                   "frac_schoolbook_basis": r4 * modexp_imad(b4, WINDOW, 1) / peak,
+                   "parity": "tests/test_gpu_parity.py::test_config4_full_batch_sampled (same inputs)"}
+        del dN4, dB4, dE4, Np4, R24, ws4, o4
+
     extra = {}
     if modmul:
         extra["modmul"] = modmul
+    if config4:
+        extra["config4"] = config4
     if c5:  # parity on the seeded 4096-element subset of the global batch + G-invariant digest
         import oracle as O
 
@@ -433,6 +468,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-config4", action="store_true", help="skip the extra config-4 (4096-bit) measurement")
     ap.add_argument("--workload", default="config3", choices=["config3", "config5"],
                     help="config3: 2^18 operands per GPU (weak scaling, the default); config5: one 2^22 batch "
                          "split across the GPUs (strong scaling), oracle subset + G-invariant digest")

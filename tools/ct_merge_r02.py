@@ -8,7 +8,11 @@ import sys
 G = "gpurun_out"
 P = "profiles/r02_ct_evidence.json"
 TAGS = {"reg1024": "k_modexp_reg<32>, register-resident CIOS with squaring rows, 1024 bits, 18944 operands",
-        "cios2048": "k_modexp<16,2,4,0>, block-engine CIOS with squaring rows, 2048 bits, 18944 operands"}
+        "cios2048": "k_modexp<16,2,4,0>, block-engine CIOS with squaring rows, 2048 bits, 18944 operands",
+        "w384": "mpb_w384::k_modexp<16,1,4,0>, one-wave 128-thread-per-SM shape of the 384-thread instance, 2048 bits, "
+                "18944 operands",
+        "w448": "mpb_w448::k_modexp<16,1,8,0>, one 448-thread CTA per SM (config 4), 4096 bits, 65536 operands"}
+TAGS = {t: TAGS[t] for t in (sys.argv[1:] or TAGS)}
 ct = json.load(open(P))
 for tag, what in TAGS.items():
     per = {}
@@ -27,4 +31,4 @@ for tag, what in TAGS.items():
     ct[tag] = {"kernel": what, "classes": per,
                "counts_identical_across_classes": all(len({per[c][k] for c in per}) == 1 for k in keys)}
 json.dump(ct, open(P, "w"), indent=1)
-print(json.dumps({k: v["counts_identical_across_classes"] for k, v in ct.items()}))
+print(json.dumps({k: v.get("counts_identical_across_classes") for k, v in ct.items() if isinstance(v, dict)}))
