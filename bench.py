@@ -18,6 +18,10 @@ collective; weak scaling).  --workload config5: one 2^22 batch split into contig
 digest of all outputs in the line (G-invariance across runs with 1/2/4/8 GPUs).
 `--impl reference` times the plain CPU oracle (oracle/, test infrastructure) on the host
 cores on bounded samples of the same workload -- the reference arm of this tier.
+Extra keys, measured on rank 0 AFTER the timed region and outside it: `modmul` (config 2 at 2048
+bits: MontMul / MontSqr per second, 2^20 operands) and `config4` (4096-bit modexp, 2^16 operands,
+the one-CTA-per-SM instance; `--no-config4` skips it).  In an ncu launch list of this command those
+are the k_mont_mul and mpb_w448::k_modexp launches; the step is k_modexp<16, 1, 4, 0, 3>.
 Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
