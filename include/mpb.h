@@ -113,7 +113,10 @@ size_t mont_batch_workspace(size_t count, int bits);
  * For >= 3072-bit operands, small batches run with 8, 4 or 2 lanes of a warp per operand (8 while
  * 8*count <= SMs*128, 4 while 4*count <= SMs*256, 2 while 2*count <= SMs*128), block products of
  * every block column split between the lanes and their windows summed by shuffles (the result is
- * the same; only the schedule differs). */
+ * the same; only the schedule differs).  A batch that fits one wave on the device (count <= SMs*384,
+ * or SMs*448 at 4096 / 4108 bits) runs one thread per operand as one CTA of 32*ceil(ceil(count/SMs)/32)
+ * threads per SM, the same kernel code compiled for that block size; the
+ * environment variable MPB_ONEWAVE=0, read once per process, disables this (tests, A/B). */
 int mont_batch_modexp_ct(const uint32_t* N, const uint32_t* Nprime, const uint32_t* R2, const uint32_t* base,
                          const uint32_t* exp, uint32_t* out, size_t count, int bits, int window, int redc,
                          int algo, void* workspace, size_t workspace_bytes, void* stream);
