@@ -107,6 +107,16 @@ int reg_policy() {
     return v;
 }
 
+// MPB_REG_TRUNC=1 runs stand-alone 1024-bit truncated MontMul / MontSqr on the register-resident
+// truncated kernel (k_mont_mul_rtr) instead of the block engine (A/B until measured)
+int reg_trunc_policy() {
+    static int v = [] {
+        const char* e = getenv("MPB_REG_TRUNC");
+        return e ? atoi(e) : 0;
+    }();
+    return v;
+}
+
 // The library's own stream-ordered memory pool for the current device (mpb_modexp_host), created
 // once per device with an unlimited release threshold so repeated calls reuse their allocation;
 // the device's default pool (and every other cudaMallocAsync user in the process) is untouched.
@@ -261,6 +271,11 @@ static int mont_op(const uint32_t* a, const uint32_t* b, const uint32_t* N, cons
     if (redc == MPB_REDC_CIOS && L == 32 && reg_policy() != 0) {  // 1024 bits: register-resident CIOS
         if (!mpb::launch_mont_mul_reg(a, sqr ? a : b, N, NP, c, count, bits, (cudaStream_t)stream))
             return fail(MPB_ECUDA, "launch_mont_mul_reg: launch refused");
+        return check_launch();
+    }
+    if (redc == MPB_REDC_TRUNCATED && L == 32 && reg_trunc_policy() > 0) {  // opt-in (A/B): register truncated
+        if (!mpb::launch_mont_mul_rtr(a, sqr ? a : b, N, NP, c, count, bits, sqr, (cudaStream_t)stream))
+            return fail(MPB_ECUDA, "launch_mont_mul_rtr: launch refused");
         return check_launch();
     }
     return dispatch_L(L, [&](auto Ci, int nb) {

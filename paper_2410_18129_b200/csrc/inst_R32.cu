@@ -208,6 +208,47 @@ __global__ void __launch_bounds__(kThreads, MPB_REG_MINB) k_mont_mul_reg(
     stb<L>(arr(c, count, k), 0, y);
 }
 
+// Stand-alone TRUNCATED MontMul / MontSqr at L = 32 (mont_batch_mul / mont_batch_sqr, redc =
+// truncated): reg::montmul_trunc (alg:trunc_montred, with Theorem 2's correction at word
+// granularity), one operation per thread, squaring and multiplication as separate instantiations
+// (SQR compile-time).  Per-thread shared memory: the a operand, N, N', T's high half.
+template <int L, bool SQR>
+__global__ void __launch_bounds__(kThreads, MPB_REG_MINB) k_mont_mul_rtr(
+    const uint32_t* __restrict__ a, const uint32_t* __restrict__ b, const uint32_t* __restrict__ N,
+    const uint32_t* __restrict__ NP, uint32_t* __restrict__ c, size_t count) {
+    const size_t k = tid_global();
+    if (k >= count) return;
+    constexpr int Q4 = L / 4;
+    constexpr int SL = L * kThreads;
+    extern __shared__ __align__(16) uint32_t smem_a[];
+    uint32_t* const sa = smem_a + threadIdx.x;
+    uint32_t* const sn = sa + SL;
+    uint32_t* const snp = sa + 2 * SL;
+    uint32_t* const sth = sa + 3 * SL;
+    auto to_slot = [&](uint32_t* slot, const Arr& A) {
+#pragma unroll
+        for (int q = 0; q < Q4; q++) {
+            const uint4 v = A.ld(q);
+            slot[(4 * q) * kThreads] = v.x;
+            slot[(4 * q + 1) * kThreads] = v.y;
+            slot[(4 * q + 2) * kThreads] = v.z;
+            slot[(4 * q + 3) * kThreads] = v.w;
+        }
+    };
+    to_slot(sa, arr(a, count, k));
+    to_slot(sn, arr(N, count, k));
+    to_slot(snp, arr(NP, count, k));
+    auto aw = [&](int i) { return sa[i * kThreads]; };
+    auto nw = [&](int j) { return sn[j * kThreads]; };
+    auto npw = [&](int j) { return snp[j * kThreads]; };
+    auto thw = [&](int i, uint32_t v) { sth[i * kThreads] = v; };
+    auto thr = [&](int i) { return sth[i * kThreads]; };
+    uint32_t bb[L], y[L];
+    ldb<L>(arr(SQR ? a : b, count, k), 0, bb);
+    reg::montmul_trunc<L>(SQR, aw, bb, npw, nw, thw, thr, y);
+    stb<L>(arr(c, count, k), 0, y);
+}
+
 // Register-resident TRUNCATED exponentiation at L = 32 (mont_batch_modexp_ct, redc = truncated):
 // reg::montmul_trunc (alg:trunc_montred + Theorem 2 at word granularity) as MontSqr and MontMul
 // instances, one call site each, inside the same flat public schedule as k_modexp_reg.  Per-thread
@@ -317,6 +358,25 @@ bool launch_modexp_rtr(const uint32_t* N, const uint32_t* NP, const uint32_t* R2
     if (cudaFuncSetAttribute(k_modexp_rtr<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) != cudaSuccess)
         return false;
     k_modexp_rtr<32><<<g, kThreads, sm, s>>>(N, NP, R2, base, exp, out, count, bits, window, ws);
+    return true;
+}
+
+bool launch_mont_mul_rtr(const uint32_t* a, const uint32_t* b, const uint32_t* N, const uint32_t* NP, uint32_t* c,
+                         size_t count, int bits, bool sqr, cudaStream_t s) {
+    if (4 * ((bits + 127) / 128) != 32) return false;
+    const unsigned g = (unsigned)((count + kThreads - 1) / kThreads);
+    const size_t sm = (size_t)kThreads * 32 * 4 * 4;  // a, N, N', T_high
+    if (sqr) {
+        if (cudaFuncSetAttribute(k_mont_mul_rtr<32, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
+            cudaSuccess)
+            return false;
+        k_mont_mul_rtr<32, true><<<g, kThreads, sm, s>>>(a, a, N, NP, c, count);
+    } else {
+        if (cudaFuncSetAttribute(k_mont_mul_rtr<32, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) !=
+            cudaSuccess)
+            return false;
+        k_mont_mul_rtr<32, false><<<g, kThreads, sm, s>>>(a, b, N, NP, c, count);
+    }
     return true;
 }
 

@@ -71,6 +71,9 @@ bool launch_modexp_rtr(const uint32_t* N, const uint32_t* NP, const uint32_t* R2
                        cudaStream_t s);
 bool launch_mont_mul_reg(const uint32_t* a, const uint32_t* b, const uint32_t* N, const uint32_t* NP, uint32_t* c,
                          size_t count, int bits, cudaStream_t s);
+// stand-alone register-resident TRUNCATED MontMul / MontSqr for L = 32 (inst_R32.cu); false if L != 32
+bool launch_mont_mul_rtr(const uint32_t* a, const uint32_t* b, const uint32_t* N, const uint32_t* NP, uint32_t* c,
+                         size_t count, int bits, bool sqr, cudaStream_t s);
 
 // scratch blocks of the Karatsuba product (mirror of mp_kara.cuh kara_scratch_blocks)
 inline int kara_scratch_blocks_host(int nb, int level) {
