@@ -984,6 +984,38 @@ def test_modexp_onewave_instances(mpb):
         assert np.array_equal(out[idx], O.batch_modexp(base[idx], exp[idx], bits, N[idx])), (bits, count, redc)
 
 
+_RTR_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+from paper_2410_18129_b200 import inputs as I, mpb
+N, x, y = I.montmul_inputs(config=2, count=301, bits=1024)
+dN, dx, dy = (mpb.to_device(v) for v in (N, x, y))
+Np, _ = mpb.mont_batch_setup(dN, 1024)
+print(mpb.to_host(mpb.mont_batch_mul(dx, dy, dN, Np, 1024, 1)).tobytes().hex())
+print(mpb.to_host(mpb.mont_batch_sqr(dx, dN, Np, 1024, 1)).tobytes().hex())
+"""
+
+
+def test_mont_ops_register_truncated_kernel(mpb):
+    """The opt-in stand-alone register-resident truncated MontMul / MontSqr at 1024 bits
+    (k_mont_mul_rtr, MPB_REG_TRUNC=1 in a subprocess) against the oracle on every operand."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, "-c", _RTR_SCRIPT % root], env=dict(os.environ, MPB_REG_TRUNC="1"),
+                         capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    mul_hex, sqr_hex = [l for l in res.stdout.splitlines() if l.strip()]
+    N, x, y = I.montmul_inputs(config=2, count=301, bits=1024)
+    L = I.limbs_for_bits(1024)
+    got_mul = np.frombuffer(bytes.fromhex(mul_hex), dtype=np.uint32).reshape(301, L)
+    got_sqr = np.frombuffer(bytes.fromhex(sqr_hex), dtype=np.uint32).reshape(301, L)
+    assert np.array_equal(got_mul, O.batch_montmul(x, y, N))
+    assert np.array_equal(got_sqr, O.batch_montmul(x, x, N))
+
+
 # ----------------------------------------------------------------------- fuzz
 def test_fuzz_shapes(mpb):
     """Seeded random shapes: widths 64..8192 bits (every block size C = 16, 12, 8, 4 and odd block
