@@ -984,7 +984,7 @@ def test_modexp_onewave_instances(mpb):
         assert np.array_equal(out[idx], O.batch_modexp(base[idx], exp[idx], bits, N[idx])), (bits, count, redc)
 
 
-_RTR_SCRIPT = r"""
+_RTR_OPS_SCRIPT = r"""
 import sys, numpy as np
 sys.path.insert(0, %r)
 from paper_2410_18129_b200 import inputs as I, mpb
@@ -1004,7 +1004,7 @@ def test_mont_ops_register_truncated_kernel(mpb):
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    res = subprocess.run([sys.executable, "-c", _RTR_SCRIPT % root], env=dict(os.environ, MPB_REG_TRUNC="1"),
+    res = subprocess.run([sys.executable, "-c", _RTR_OPS_SCRIPT % root], env=dict(os.environ, MPB_REG_TRUNC="1"),
                          capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stderr[-2000:]
     mul_hex, sqr_hex = [l for l in res.stdout.splitlines() if l.strip()]
